@@ -1,0 +1,365 @@
+#!/usr/bin/env python3
+"""Benchmark of the Garfield GAR hot path on B200.
+
+Metric (BASELINE.json): GAR throughput in GB/s of gradients, n*d*4 bytes per
+rule / time, plus the dominant kernel's fraction of the HBM roofline.
+
+A step is one pass of the whole hot path (every row of SURVEY.md §8(a)) over
+the workload: Average, Median, trimmed mean, Krum, Multi-Krum and Bulyan, each
+aggregating the same n resident gradients.  Default workload = BASELINE.json
+configs[2] (ResNet-50-sized gradients, n=31, f=7, d=25,557,032: the config the
+north_star targets and scales to 8 GPUs); inputs (3.17 GB) exceed the 126 MB
+L2, so no flush is needed between steps.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (d-sharded, NCCL)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+RULES = ("average", "median", "trimmed_mean", "krum", "multi_krum", "bulyan")
+KRUM = ("krum", "multi_krum", "bulyan")
+METRIC = "GAR throughput GB/s of gradients (n*d*4B/time), all six GARs per step"
+FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback (used only if MEASURED_PEAKS.json is absent)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C3", help="C1..C4 or sweep:<n>")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--output", default="replicated", choices=["replicated", "sharded"],
+                    help="N>1: all-gather the aggregate to every rank (north_star) or keep it d-sharded")
+    return ap.parse_args()
+
+
+def workload(name):
+    if name.startswith("sweep:"):
+        return synth.sweep_config(int(name.split(":")[1]))
+    return synth.CONFIGS[name]
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def rule_bytes(rule, n, f, d):
+    """Algorithmic HBM bytes of one aggregation."""
+    if rule in ("average", "median", "trimmed_mean"):
+        return 4 * d * (n + 1)
+    if rule == "krum":
+        return 4 * d * (n + 2)
+    if rule == "multi_krum":
+        return 4 * d * (n + (n - f - 2) + 1)
+    return 4 * d * (n + (n - 2 * f) + 1)
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [l.split(",") for l in open(self.path).read().strip().splitlines()]
+            rows = [[c.strip() for c in r] for r in rows if len(r) >= 9]
+            sm = [float(r[1]) for r in rows]
+            mx = max(float(r[2]) for r in rows)
+            reasons = set()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for r in rows:
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower().startswith("active"):
+                        reasons.add(nm)
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                    "samples": len(rows)}
+        except Exception as e:  # pragma: no cover
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": str(e)}
+        finally:
+            try:
+                os.remove(self.path)
+            except OSError:
+                pass
+
+
+def traffic_from_profiles(kernel_class):
+    """dram bytes per launch of the dominant kernel, from the committed ncu capture summary."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(kernel_class)
+    except Exception:
+        return None
+
+
+# ============================================================== our implementation
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_05888_b200 as gar
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = workload(args.workload)
+    n, f, d = cfg.n, cfg.f, cfg.d
+    lo, hi = synth.shard_bounds(d, rank, world) if world > 1 else (0, d)
+    dl = hi - lo
+    X = synth.make_gradients(n, f, dl, seed=synth.BASE_SEED + 2 + 1000 * rank, device=dev)
+    torch.cuda.synchronize()
+
+    aggs = {r: gar.init(r, n, f) for r in RULES}
+    outs = {r: torch.empty(dl, dtype=torch.float32, device=dev) for r in RULES}
+    per = synth.shard_bounds(d, 0, world)[1] if world > 1 else d
+    full = {r: torch.empty(per * world, dtype=torch.float32, device=dev) for r in RULES} if world > 1 else None
+    padded = torch.zeros(per, dtype=torch.float32, device=dev) if world > 1 else None
+    ws = torch.empty(max(gar.gar_workspace_bytes(r, n, f, dl) for r in KRUM), dtype=torch.uint8, device=dev)
+    G = torch.empty((n, n), dtype=torch.float64, device=dev)
+    idx = {r: torch.empty(64, dtype=torch.int32, device=dev) for r in KRUM}
+    stream = torch.cuda.current_stream(dev)
+
+    segs = []          # (kernel class, rule, start event, end event)
+
+    def mark():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    def step(record):
+        for r in ("average", "median", "trimmed_mean"):
+            a = mark() if record else None
+            aggs[r].aggregate(X, out=outs[r], d=dl)
+            if record:
+                segs.append(("coord_select", r, a, mark()))
+            if world > 1 and args.output == "replicated":
+                padded[:dl].copy_(outs[r])
+                dist.all_gather_into_tensor(full[r], padded)
+        for r in KRUM:
+            a = mark() if record else None
+            gar.gar_gram_partial(X, G, ws, d=dl)
+            b = mark() if record else None
+            if world > 1:
+                dist.all_reduce(G)
+            c = mark() if record else None
+            gar.gar_select_from_gram(r, G, n, f, 0, idx[r])
+            e1 = mark() if record else None
+            gar.gar_combine(r, X, f, 0, idx[r], outs[r], d=dl)
+            if record:
+                e2 = mark()
+                segs.extend([("gram", r, a, b), ("exchange", r, b, c), ("select", r, c, e1),
+                             ("coord_select", r, e1, e2)])
+            if world > 1 and args.output == "replicated":
+                padded[:dl].copy_(outs[r])
+                dist.all_gather_into_tensor(full[r], padded)
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        t0 = mark()
+        for _ in range(args.steps):
+            step(True)
+        t1 = mark()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    # per-segment device times
+    cls_ms, rule_ms = {}, {r: 0.0 for r in RULES}
+    for cls, r, a, b in segs:
+        t = a.elapsed_time(b)
+        cls_ms[cls] = cls_ms.get(cls, 0.0) + t
+        rule_ms[r] += t
+    if world > 1:
+        t = torch.tensor([ms] + [rule_ms[r] for r in RULES], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+        rule_ms = {r: float(t[1 + i]) for i, r in enumerate(RULES)}
+
+    # ---- e2e through the public API with host buffers (pinned), copies in the timed region
+    e2e = None
+    if args.e2e_steps > 0:
+        host_x = torch.empty(X.shape, dtype=torch.float32, pin_memory=True)
+        host_x.copy_(X)
+        host_out = {r: torch.empty(dl, dtype=torch.float32, pin_memory=True) for r in RULES}
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a = mark()
+        for _ in range(args.e2e_steps):
+            X.copy_(host_x, non_blocking=True)
+            for r in RULES:
+                aggs[r].aggregate(X, out=outs[r], d=dl)
+                host_out[r].copy_(outs[r], non_blocking=True)
+        b = mark()
+        torch.cuda.synchronize()
+        e2e_ms = a.elapsed_time(b) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t[0])
+        e2e = {"value": round(len(RULES) * n * d * 4 / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": int(X.numel() * 4 * world),
+               "d2h_bytes_per_step": int(len(RULES) * dl * 4 * world),
+               "path": "Aggregator.aggregate (gar_aggregate_ex) per rule, inputs H2D from pinned host each step"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak, peak_src = peaks()
+    ms_step = ms / args.steps
+    grad_bytes = len(RULES) * n * d * 4
+    value = grad_bytes / (ms_step * 1e-3) / 1e9
+    # dominant kernel roofline (single-GPU algorithmic bytes per launch)
+    launches = {"coord_select": 6, "gram": 3}
+    bytes_cls = {
+        "coord_select": sum(rule_bytes(r, n, f, dl) for r in ("average", "median", "trimmed_mean"))
+        + sum(4 * dl * (R + 1) for R in (1, n - f - 2, n - 2 * f)),
+        "gram": 3 * 4 * n * dl,
+    }
+    kernels = {}
+    for c in ("coord_select", "gram"):
+        t = cls_ms.get(c, 0.0) / args.steps
+        ach = bytes_cls[c] / (t * 1e-3) / 1e9 if t > 0 else 0.0
+        kernels[c] = {"ms_per_step": round(t, 4), "launches_per_step": launches[c],
+                      "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 4),
+                      "share_of_step": round(t / ms_step, 4)}
+    dom = max(kernels, key=lambda c: kernels[c]["ms_per_step"])
+    per_launch_bytes = bytes_cls[dom] / launches[dom]
+    per_rule = {}
+    for r in RULES:
+        t = rule_ms[r] / args.steps
+        per_rule[r] = {"ms": round(t, 4), "grad_gbs": round(n * d * 4 / (t * 1e-3) / 1e9, 1),
+                       "roofline_frac": round(rule_bytes(r, n, f, d) / world / (t * 1e-3) / 1e9 / peak, 4)}
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: n={n} f={f} d={d}, GARs {'/'.join(RULES)}",
+                   "n": n, "f": f, "d": d, "parallelism": f"d-sharded x{world}" if world > 1 else "single GPU",
+                   "output": args.output if world > 1 else "local",
+                   "l2": f"inputs {n * d * 4 / 1e9:.2f} GB > 126 MB L2 (no flush needed)"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": kernels[dom]["frac"],
+                     "algorithmic_bytes_per_launch": int(per_launch_bytes),
+                     "traffic": traffic_from_profiles(dom)},
+        "kernels": kernels, "per_rule": per_rule, "clocks": clk.summary(),
+        "gpu_launches": 15 * args.steps, "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, sample_d=1 << 20)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ============================================================== the oracle as the reference arm
+def oracle_step(x, f):
+    import oracle
+    for r in RULES:
+        oracle.aggregate(r, x, f)
+
+
+def cpu_baseline(cfg, sample_d):
+    import oracle
+    x = synth.make_gradients(cfg.n, cfg.f, sample_d, seed=synth.BASE_SEED + 2, ld=sample_d).numpy()
+    t = time.perf_counter()
+    oracle_step(x, cfg.f)
+    dt = time.perf_counter() - t
+    return {"value": round(len(RULES) * cfg.n * sample_d * 4 / dt / 1e9, 4), "unit": "GB/s",
+            "cores": oracle.default_threads(), "kind": "oracle",
+            "sample": f"first-draw {cfg.name} shape, n={cfg.n} f={cfg.f}, d={sample_d} coordinates, all six GARs "
+                      f"once ({dt:.2f} s)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    cfg = workload(args.workload)
+    sample_d = 1 << 18
+    x = synth.make_gradients(cfg.n, cfg.f, sample_d, seed=synth.BASE_SEED + 2, ld=sample_d).numpy()
+    for _ in range(args.warmup):
+        oracle_step(x, cfg.f)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_step(x, cfg.f)
+    dt = (time.perf_counter() - t) / args.steps
+    value = len(RULES) * cfg.n * sample_d * 4 / dt / 1e9
+    sample = (f"{cfg.name} shape n={cfg.n} f={cfg.f}, first d={sample_d} of {cfg.d} coordinates per step, "
+              f"all six GARs")
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: n={cfg.n} f={cfg.f} d={cfg.d}, GARs {'/'.join(RULES)}",
+                       "n": cfg.n, "f": cfg.f, "d": cfg.d},
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": oracle.default_threads(),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

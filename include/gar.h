@@ -1,0 +1,140 @@
+/* gar.h — libgar: the C-ABI boundary of the Garfield GAR hot path on B200.
+ *
+ * Garfield (arXiv 2010.05888) §3.3 "Statistically Robust GARs" (PAPER.md
+ * l.198-225): "A GAR is merely a function of (R^d)^q -> R^d ... these GARs wait
+ * for q vectors before applying some functions on them" (l.201-203).  The
+ * paper's aggregation module exposes two calls, init(name, n, f) and
+ * aggregate(n tensors), the device being chosen by where the inputs live
+ * (§4.1 "Aggregation").  libgar is that module for
+ * B200 (sm_100a) GPUs; every step runs in hand-written CUDA kernels.
+ *
+ * Conventions for every entry point
+ * ---------------------------------
+ *  - grads:  HOST array of n DEVICE pointers; grads[i] is worker i's gradient,
+ *            fp32[d] (or fp32[d_local] for the sharded calls), 16-byte
+ *            aligned.  The array itself is copied into kernel parameters at
+ *            call time; the caller may free it when the call returns.
+ *  - 1 <= n <= GAR_MAX_N (64), f >= 0, d >= 0.
+ *  - out:    DEVICE fp32[d], 16-byte aligned, must not alias any grads[i].
+ *  - indices_dev: DEVICE int32 array of at least GAR_MAX_N entries.
+ *  - stream: the CUDA stream all work is enqueued on (NULL = legacy default).
+ *  - Ownership: the caller owns every buffer; libgar never allocates device
+ *    memory except in gar_aggregate (7-argument convenience form), which
+ *    takes its workspace from cudaMallocAsync on `stream`.
+ *  - Argument checks run synchronously before any launch; on failure nothing
+ *    is written.  Execution is asynchronous: results are valid once `stream`
+ *    reaches the point of the call.  Launch failures return GAR_ERR_CUDA.
+ *  - No CPU fallback: host pointers in grads/out -> GAR_ERR_INVALID_ARGUMENT.
+ *  - Stateless and re-entrant; concurrent calls need separate workspaces.
+ *  - Results are bitwise deterministic for fixed inputs.
+ *
+ * Numerics (DESIGN.md §3 readings R1-R11): order statistics on canonical
+ * values (NaN -> +inf, -0 -> +0), averages as fp64 sums rounded once to fp32,
+ * squared Euclidean distances from a tensor-core Gram matrix, ties to the
+ * lower input index.
+ */
+#ifndef GARFIELD_B200_GAR_H_
+#define GARFIELD_B200_GAR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* gar_stream_t; /* == cudaStream_t */
+
+#define GAR_MAX_N 64
+
+typedef enum {
+  GAR_AVERAGE = 0,      /* PAPER.md l.146-152 (§2.2), control rule l.553-554          */
+  GAR_MEDIAN = 1,       /* coordinate-wise median, q >= 2f+1, l.207-208              */
+  GAR_TRIMMED_MEAN = 2, /* coordinate-wise trimmed mean, l.316 footnote; R6          */
+  GAR_KRUM = 3,         /* Multi-Krum with m = 1, l.210-212; R10                     */
+  GAR_MULTI_KRUM = 4,   /* average of the m smallest-score inputs, l.210-212         */
+  GAR_BULYAN = 5        /* iterated Krum + coordinate phase, l.219-225; R7, R8       */
+} gar_rule;
+
+typedef enum {
+  GAR_OK = 0,
+  GAR_ERR_INVALID_ARGUMENT = 1, /* null/host pointer, n outside [1,64], f<0, d<0, out aliases an input, bad rule */
+  GAR_ERR_QUORUM = 2,           /* n < 2f+1 (median, trimmed) | 2f+3 (Krum family) | 4f+3 (Bulyan); l.208, l.212, l.225 */
+  GAR_ERR_INVALID_M = 3,        /* Multi-Krum m outside [1, n-f-2] (l.210)                              */
+  GAR_ERR_ALIGNMENT = 4,        /* a row or out pointer not 16-byte aligned                             */
+  GAR_ERR_UNSUPPORTED = 5,      /* selection asked of a coordinate-wise rule                           */
+  GAR_ERR_WORKSPACE = 6,        /* workspace missing or smaller than gar_workspace_bytes()             */
+  GAR_ERR_CUDA = 7              /* a CUDA call or kernel launch failed                                  */
+} gar_status;
+
+/* Human-readable name of a status code (static storage). */
+const char* gar_status_string(gar_status s);
+
+/* Bytes of device workspace gar_aggregate_ex / gar_select / gar_gram_partial
+ * need for (rule, n, f, d); 0 for the coordinate-wise rules.  Pure host
+ * function (no CUDA call).  Returns 0 on invalid arguments. */
+size_t gar_workspace_bytes(gar_rule rule, int n, int f, int64_t d);
+
+/* Number of indices the selection of (rule, n, f, m) produces: Krum 1,
+ * Multi-Krum m (0 -> n-f-2), Bulyan n-2f; 0 for coordinate-wise rules or on
+ * invalid arguments.  Pure host function. */
+int gar_num_selected(gar_rule rule, int n, int f, int m);
+
+/* out = GAR_rule(grads[0..n)) over d coordinates (default m = n-f-2 for
+ * Multi-Krum).  Allocates its workspace with cudaMallocAsync on `stream`. */
+gar_status gar_aggregate(gar_rule rule, const float* const* grads, int n, int f, int64_t d,
+                         float* out, gar_stream_t stream);
+
+/* Full form.  m: Multi-Krum selection size (0 -> n-f-2; ignored by other
+ * rules).  indices_dev: optional DEVICE int32[>= n_selected] receiving the
+ * selected input indices in selection order (Krum family; may be NULL).
+ * workspace: DEVICE buffer of >= gar_workspace_bytes(rule, n, f, d) bytes
+ * (may be NULL for the coordinate-wise rules). */
+gar_status gar_aggregate_ex(gar_rule rule, const float* const* grads, int n, int f, int m,
+                            int64_t d, float* out, int32_t* indices_dev, void* workspace,
+                            size_t workspace_bytes, gar_stream_t stream);
+
+/* Selection only (Krum, Multi-Krum, Bulyan): indices in selection order —
+ * ascending (score, index) for Krum/Multi-Krum, round order for Bulyan — into
+ * indices_dev.  *n_selected_host (optional) receives the count, known
+ * without synchronising. */
+gar_status gar_select(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d,
+                      int32_t* indices_dev, int* n_selected_host, void* workspace,
+                      size_t workspace_bytes, gar_stream_t stream);
+
+/* Pairwise squared distances D (DEVICE fp64[n*n], row-major, symmetric,
+ * zero diagonal, non-finite -> +inf) from the tensor-core Gram matrix:
+ * D_ij = G_ii + G_jj - 2 G_ij with G the Gram matrix of the centred rows
+ * (row a5).  workspace as for Krum. */
+gar_status gar_distances(const float* const* grads, int n, int64_t d, double* D_dev,
+                         void* workspace, size_t workspace_bytes, gar_stream_t stream);
+
+/* ---- d-sharded building blocks (multi-GPU) -----------------
+ * A rank holding coordinates [lo, lo+d_local) of every gradient calls
+ * gar_gram_partial, sums gram_dev over ranks (NCCL all-reduce, fp64), then
+ * gar_select_from_gram (identical on every rank) and gar_combine on its slice.
+ * The centring reference of the Gram is per-coordinate, so partial Grams of
+ * disjoint coordinate slices add up to the Gram of the whole vectors. */
+
+/* gram_dev: DEVICE fp64[n*n], the Gram matrix of the centred local slice. */
+gar_status gar_gram_partial(const float* const* grads, int n, int64_t d_local, double* gram_dev,
+                            void* workspace, size_t workspace_bytes, gar_stream_t stream);
+
+/* Selection from a (summed) Gram matrix; same outputs as gar_select.
+ * workspace: >= gar_workspace_bytes(rule, n, f, 0) bytes. */
+gar_status gar_select_from_gram(gar_rule rule, const double* gram_dev, int n, int f, int m,
+                                int32_t* indices_dev, int* n_selected_host, void* workspace,
+                                size_t workspace_bytes, gar_stream_t stream);
+
+/* Combine step on a coordinate slice given the selection: Krum copies the
+ * selected row, Multi-Krum averages the m selected rows, Bulyan runs its
+ * coordinate phase over the n-2f selected rows.  indices_dev as produced by
+ * gar_select / gar_select_from_gram. */
+gar_status gar_combine(gar_rule rule, const float* const* grads, int n, int f, int m,
+                       int64_t d_local, const int32_t* indices_dev, float* out,
+                       gar_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GARFIELD_B200_GAR_H_ */

@@ -1,0 +1,188 @@
+"""ctypes binding of libgar.so (include/gar.h) — argument marshalling only.
+
+Every function here has the name of the C entry point it wraps and takes
+torch tensors (device memory) where the C call takes device pointers.  No
+step of the method runs in Python; there is no CPU fallback: if libgar.so is
+missing or was built without the kernels, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgar.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "gar.h")
+
+RULES = {"average": 0, "median": 1, "trimmed_mean": 2, "krum": 3, "multi_krum": 4, "bulyan": 5}
+STATUS = {0: "GAR_OK", 1: "GAR_ERR_INVALID_ARGUMENT", 2: "GAR_ERR_QUORUM", 3: "GAR_ERR_INVALID_M",
+          4: "GAR_ERR_ALIGNMENT", 5: "GAR_ERR_UNSUPPORTED", 6: "GAR_ERR_WORKSPACE", 7: "GAR_ERR_CUDA"}
+MAX_N = 64
+
+
+class GarError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what}: {STATUS.get(code, code)}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libgar.so not built ({LIB_PATH}); run `python -m paper_2010_05888_b200.build` "
+                          "(nvcc, sm_100a).  There is no CPU fallback.")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I, I64, SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
+    PP = ctypes.POINTER(ctypes.c_void_p)
+    IP = ctypes.POINTER(ctypes.c_int)
+    sigs = {
+        "gar_status_string": ([I], ctypes.c_char_p),
+        "gar_workspace_bytes": ([I, I, I, I64], SZ),
+        "gar_num_selected": ([I, I, I, I], I),
+        "gar_aggregate": ([I, PP, I, I, I64, P, P], I),
+        "gar_aggregate_ex": ([I, PP, I, I, I, I64, P, P, P, SZ, P], I),
+        "gar_select": ([I, PP, I, I, I, I64, P, IP, P, SZ, P], I),
+        "gar_distances": ([PP, I, I64, P, P, SZ, P], I),
+        "gar_gram_partial": ([PP, I, I64, P, P, SZ, P], I),
+        "gar_select_from_gram": ([I, P, I, I, I, P, IP, P, SZ, P], I),
+        "gar_combine": ([I, PP, I, I, I, I64, P, P, P], I),
+    }
+    for name, (args, res) in sigs.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    return L
+
+
+lib = _load()
+
+
+def header_functions() -> list[str]:
+    """Entry points declared in include/gar.h (for the export test)."""
+    with open(HEADER) as fh:
+        src = fh.read()
+    return sorted(set(re.findall(r"^(?:gar_status|size_t|int|const char\*)\s+(gar_\w+)\s*\(", src, re.M)))
+
+
+# ------------------------------------------------------------------ marshalling
+def rule_id(rule) -> int:
+    if isinstance(rule, str):
+        if rule not in RULES:
+            raise ValueError(f"unknown GAR {rule!r}; expected one of {sorted(RULES)}")
+        return RULES[rule]
+    return int(rule)
+
+
+def row_pointers(grads, d: int | None = None):
+    """(ctypes void* array, n, d) from a list of 1-D fp32 CUDA tensors or a
+    2-D [n, ld] fp32 CUDA tensor with unit column stride."""
+    if isinstance(grads, torch.Tensor):
+        if grads.dim() != 2:
+            raise ValueError("a gradient matrix must be 2-D [n, ld]")
+        rows = [grads[i] for i in range(grads.shape[0])]
+    else:
+        rows = list(grads)
+    n = len(rows)
+    if not 1 <= n <= MAX_N:
+        raise ValueError(f"n = {n} outside [1, {MAX_N}]")
+    dev = rows[0].device
+    for r in rows:
+        if r.dtype != torch.float32:
+            raise TypeError("gradients must be float32")
+        if r.device != dev or r.device.type != "cuda":
+            raise ValueError("gradients must all live on the same CUDA device (no CPU fallback)")
+        if r.dim() != 1 or (r.numel() > 1 and r.stride(0) != 1):
+            raise ValueError("each gradient must be a contiguous 1-D view")
+    if d is None:
+        d = min(r.numel() for r in rows)
+    elif any(r.numel() < d for r in rows):
+        raise ValueError("a gradient is shorter than d")
+    arr = (ctypes.c_void_p * n)(*[r.data_ptr() for r in rows])
+    return arr, n, d, dev
+
+
+def stream_handle(device, stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def check(code: int, what: str):
+    if code != 0:
+        raise GarError(code, what)
+
+
+# ------------------------------------------------------------------ same names as the C ABI
+def gar_status_string(code: int) -> str:
+    return lib.gar_status_string(code).decode()
+
+
+def gar_workspace_bytes(rule, n: int, f: int, d: int) -> int:
+    return int(lib.gar_workspace_bytes(rule_id(rule), n, f, d))
+
+
+def gar_num_selected(rule, n: int, f: int, m: int = 0) -> int:
+    return int(lib.gar_num_selected(rule_id(rule), n, f, m))
+
+
+def gar_aggregate(rule, grads, f: int, out: torch.Tensor, d: int | None = None, stream=None):
+    arr, n, d, dev = row_pointers(grads, d)
+    check(lib.gar_aggregate(rule_id(rule), arr, n, f, d, _ptr(out), stream_handle(dev, stream)),
+          "gar_aggregate")
+    return out
+
+
+def gar_aggregate_ex(rule, grads, f: int, m: int, out: torch.Tensor, indices=None, workspace=None,
+                     d: int | None = None, stream=None):
+    arr, n, d, dev = row_pointers(grads, d)
+    wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    check(lib.gar_aggregate_ex(rule_id(rule), arr, n, f, m, d, _ptr(out), _ptr(indices), _ptr(workspace),
+                               wsb, stream_handle(dev, stream)), "gar_aggregate_ex")
+    return out
+
+
+def gar_select(rule, grads, f: int, m: int, indices: torch.Tensor, workspace: torch.Tensor,
+               d: int | None = None, stream=None) -> int:
+    arr, n, d, dev = row_pointers(grads, d)
+    nsel = ctypes.c_int(0)
+    check(lib.gar_select(rule_id(rule), arr, n, f, m, d, _ptr(indices), ctypes.byref(nsel), _ptr(workspace),
+                         workspace.numel() * workspace.element_size(), stream_handle(dev, stream)),
+          "gar_select")
+    return nsel.value
+
+
+def gar_distances(grads, D: torch.Tensor, workspace: torch.Tensor, d: int | None = None, stream=None):
+    arr, n, d, dev = row_pointers(grads, d)
+    check(lib.gar_distances(arr, n, d, _ptr(D), _ptr(workspace), workspace.numel() * workspace.element_size(),
+                            stream_handle(dev, stream)), "gar_distances")
+    return D
+
+
+def gar_gram_partial(grads, gram: torch.Tensor, workspace: torch.Tensor, d: int | None = None, stream=None):
+    arr, n, d, dev = row_pointers(grads, d)
+    check(lib.gar_gram_partial(arr, n, d, _ptr(gram), _ptr(workspace),
+                               workspace.numel() * workspace.element_size(), stream_handle(dev, stream)),
+          "gar_gram_partial")
+    return gram
+
+
+def gar_select_from_gram(rule, gram: torch.Tensor, n: int, f: int, m: int, indices: torch.Tensor,
+                         stream=None) -> int:
+    nsel = ctypes.c_int(0)
+    check(lib.gar_select_from_gram(rule_id(rule), _ptr(gram), n, f, m, _ptr(indices), ctypes.byref(nsel),
+                                   None, 0, stream_handle(gram.device, stream)), "gar_select_from_gram")
+    return nsel.value
+
+
+def gar_combine(rule, grads, f: int, m: int, indices: torch.Tensor, out: torch.Tensor, d: int | None = None,
+                stream=None):
+    arr, n, d, dev = row_pointers(grads, d)
+    check(lib.gar_combine(rule_id(rule), arr, n, f, m, d, _ptr(indices), _ptr(out),
+                          stream_handle(dev, stream)), "gar_combine")
+    return out

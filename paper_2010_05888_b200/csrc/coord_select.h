@@ -1,0 +1,23 @@
+// coord_select.h — internal launch interface of the coordinate-selection kernel.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gar {
+
+enum CoordMode { kModeAverage = 0, kModeMedian = 1, kModeTrimmed = 2, kModeBulyan = 3 };
+
+struct CoordLaunch {
+  const float* const* rows;   // host array of n device row pointers
+  int n;                      // number of input rows
+  const int32_t* idx;         // device: R selected indices (any order) or nullptr
+  int R;                      // rows consumed per coordinate (n, m or theta)
+  int f;                      // trim per side / Bulyan f
+  int64_t d;                  // coordinates
+  float* out;                 // device fp32[d]
+  int num_sms;
+};
+
+cudaError_t launch_coord_select(int mode, const CoordLaunch& L, cudaStream_t stream);
+
+}  // namespace gar

@@ -1,0 +1,266 @@
+#pragma once
+// coord_select_impl.cuh — the per-coordinate selection kernel (rows a1-a4, a8, a9 of
+// DESIGN.md §1): Average, Median, trimmed mean, Multi-Krum/Krum combine and
+// the Bulyan coordinate phase.  Product code for sm_100a.
+//
+// Dataflow (one persistent CTA per SM slot):
+//   producer warp : one elected lane streams [R rows x T coords] tiles into a
+//                   multi-stage shared-memory ring with 1D TMA bulk copies
+//                   (cp.async.bulk ... mbarrier::complete_tx), L2 evict_first;
+//   8 consumer warps: thread c owns column c of the tile, reads its R values
+//                   from shared memory (conflict-free), canonicalises them
+//                   (R1), runs a straight-line FMNMX network from
+//                   networks.cuh, accumulates averages in fp64 (R2) and writes
+//                   one coalesced fp32 per coordinate.
+// HBM traffic is the algorithmic minimum: every input byte read once, every
+// output byte written once.
+#include <cfloat>
+#include <cstdint>
+
+#include "common.cuh"
+#include "coord_select.h"
+#include "networks.cuh"
+
+namespace gar {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kTile = kConsumerWarps * 32;       // coordinates per tile
+constexpr int kThreads = kTile + 32;             // + 1 producer warp
+
+struct CoordParams {
+  RowPtrs rows;
+  const int32_t* idx;   // nullptr: rows 0..R-1; else R selected input indices
+  float* out;
+  int64_t d;
+  int R;                // rows consumed per coordinate
+  int f;                // trimmed mean: trim per side; Bulyan: declared f
+  int stages;
+  int64_t num_tiles;
+};
+
+// ---------------------------------------------------------------- per-mode math
+// Average over R values in index order, fp64 (R2).
+__device__ __forceinline__ float avg_column(const float* col, int R, int stride) {
+  double s = 0.0;
+  for (int i = 0; i < R; ++i) s += static_cast<double>(col[i * stride]);
+  return static_cast<float>(s / R);
+}
+
+template <int N>
+__device__ __forceinline__ float median_column(float* v) {
+  gar_net::median_net<N>(v);
+  if constexpr (N % 2 == 1) {
+    return v[(N - 1) / 2];
+  } else {
+    return static_cast<float>((static_cast<double>(v[N / 2 - 1]) + static_cast<double>(v[N / 2])) * 0.5);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ float trimmed_column(float* v, int f) {
+  gar_net::sort_net<N>(v);
+  double s = 0.0;
+#pragma unroll
+  for (int t = 0; t < N; ++t)
+    if (t >= f && t < N - f) s += static_cast<double>(v[t]);
+  return static_cast<float>(s / (N - 2 * f));
+}
+
+__device__ __forceinline__ float closeness(float y, float med) {
+  return (y == med) ? 0.0f : fabsf(__fsub_rn(y, med));
+}
+
+// Bulyan coordinate phase over THETA canonical values (positions = ascending
+// input index).  Keeps the beta = THETA - 2f values with the smallest
+// (closeness, index) (R8) and averages them in ascending order (R2).
+//
+// In value-sorted order the kept multiset is a window [s*, s*+beta): closeness
+// decreases towards the median from the left and increases from the right, so
+// "shift the window right by one" (drop v[s], take v[s+beta]) is a monotone
+// predicate and s* = s_min + #{s : c(v[s+beta]) < c(v[s])}.  A closeness tie
+// between two DIFFERENT values needs the input indices: those (rare) columns
+// take the exact rank-count path over the index-ordered values.
+// The sorted column is parked in the CTA's shared-memory slot so the
+// runtime-offset reads (beta depends on the runtime f) are plain LDS.
+template <int THETA>
+__device__ __forceinline__ float bulyan_column(float* v, float* col, int stride, int f,
+                                               const float* const* rowp, int64_t gidx) {
+  const int beta = THETA - 2 * f;
+  gar_net::sort_net<THETA>(v);
+#pragma unroll
+  for (int t = 0; t < THETA; ++t) col[t * stride] = v[t];
+  constexpr int h = (THETA - 1) / 2;
+  float med;
+  if constexpr (THETA % 2 == 1) {
+    med = v[h];
+  } else {
+    med = static_cast<float>((static_cast<double>(v[h]) + static_cast<double>(v[h + 1])) * 0.5);
+  }
+  constexpr int h_hi = (THETA % 2 == 1) ? h : h + 1;
+  const int s_min = max(0, h - beta + 1);
+  const int s_max = min(THETA - beta, h_hi);
+  int shift = 0;
+  bool tie = false;
+  for (int s = s_min; s < s_max; ++s) {
+    const float left = col[s * stride], right = col[(s + beta) * stride];
+    const float cl = closeness(left, med), cr = closeness(right, med);
+    shift += (cr < cl) ? 1 : 0;
+    tie |= (cr == cl) && (right != left);
+  }
+  int start = s_min + shift;
+  if (tie) {
+    // exact path: kept_t  <=>  #{u : (c_u, u) < (c_t, t)} < beta, index order
+    int p = 0, kL = 0;
+    for (int t = 0; t < THETA; ++t) {
+      const float yt = canon(__ldg(rowp[t] + gidx));
+      const float ct = closeness(yt, med);
+      int rank = 0;
+      for (int u = 0; u < THETA; ++u) {
+        const float cu = closeness(canon(__ldg(rowp[u] + gidx)), med);
+        rank += (cu < ct || (cu == ct && u < t)) ? 1 : 0;
+      }
+      p += (yt < med) ? 1 : 0;
+      kL += (rank < beta && yt < med) ? 1 : 0;
+    }
+    start = p - kL;
+  }
+  double acc = 0.0;
+  for (int j = 0; j < beta; ++j) acc += static_cast<double>(col[(start + j) * stride]);
+  return static_cast<float>(acc / beta);
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int MODE, int N>
+__global__ void __launch_bounds__(kThreads, 2) coord_select_kernel(const __grid_constant__ CoordParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int R = (N > 0) ? N : p.R;
+  const int stages = p.stages;
+  float* tiles = reinterpret_cast<float*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + size_t(stages) * R * kTile * sizeof(float));
+  uint64_t* empty = full + stages;
+  __shared__ const float* rowp[GAR_MAX_N];
+  __shared__ int sel_s[GAR_MAX_N];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    if (p.idx) {
+      // selected rows in ascending input-index order (R2, R8 tie order)
+      for (int r = 0; r < R; ++r) {
+        int v = p.idx[r], t = r;
+        while (t > 0 && sel_s[t - 1] > v) { sel_s[t] = sel_s[t - 1]; --t; }
+        sel_s[t] = v;
+      }
+      for (int r = 0; r < R; ++r) rowp[r] = p.rows.p[sel_s[r]];
+    } else {
+      for (int r = 0; r < R; ++r) rowp[r] = p.rows.p[r];
+    }
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int64_t d = p.d;
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------ producer (TMA bulk)
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        const int64_t start = tile * kTile;
+        const int cnt = static_cast<int>((d - start < kTile ? d - start : int64_t(kTile)));
+        const uint32_t bytes = static_cast<uint32_t>(cnt & ~3) * 4u;
+        mbar_arrive_expect_tx(&full[stage], bytes * R);
+        if (bytes) {
+          float* dst = tiles + size_t(stage) * R * kTile;
+          for (int r = 0; r < R; ++r) bulk_g2s(dst + r * kTile, rowp[r] + start, bytes, &full[stage], pol);
+        }
+        if (++stage == stages) { stage = 0; phase ^= 1; }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------- consumers
+  int stage = 0;
+  uint32_t phase = 0;
+  const int c = threadIdx.x;
+  for (int64_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    mbar_wait(&full[stage], phase);
+    const int64_t start = tile * kTile;
+    const int cnt = static_cast<int>((d - start < kTile ? d - start : int64_t(kTile)));
+    const int bulk_cnt = cnt & ~3;
+    float* col = tiles + size_t(stage) * R * kTile + c;
+    if (c >= bulk_cnt && c < cnt) {
+      // ragged tail (< 4 coordinates): not bulk-copied, fetch directly
+      for (int r = 0; r < R; ++r) col[r * kTile] = __ldg(rowp[r] + start + c);
+    }
+    if (c < cnt) {
+      float res;
+      if constexpr (MODE == kModeAverage) {
+        res = avg_column(col, R, kTile);
+      } else {
+        float v[N > 0 ? N : 1];
+#pragma unroll
+        for (int r = 0; r < N; ++r) v[r] = canon(col[r * kTile]);
+        if constexpr (MODE == kModeMedian) {
+          res = median_column<N>(v);
+        } else if constexpr (MODE == kModeTrimmed) {
+          res = trimmed_column<N>(v, p.f);
+        } else {
+          res = bulyan_column<N>(v, col, kTile, p.f, rowp, start + c);
+        }
+      }
+      p.out[start + c] = res;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == stages) { stage = 0; phase ^= 1; }
+  }
+}
+
+// ---------------------------------------------------------------- host side
+template <int MODE, int N>
+inline cudaError_t launch_mode(const CoordLaunch& L, cudaStream_t stream) {
+  CoordParams p;
+  for (int i = 0; i < GAR_MAX_N; ++i) p.rows.p[i] = (i < L.n) ? L.rows[i] : nullptr;
+  p.idx = L.idx;
+  p.out = L.out;
+  p.d = L.d;
+  p.R = L.R;
+  p.f = L.f;
+  const size_t stage_bytes = size_t(L.R) * kTile * sizeof(float);
+  int stages = static_cast<int>((96 * 1024) / stage_bytes);
+  stages = max(2, min(8, stages));
+  p.stages = stages;
+  p.num_tiles = (L.d + kTile - 1) / kTile;
+  const size_t smem = stages * stage_bytes + 2 * stages * sizeof(uint64_t);
+  auto kern = coord_select_kernel<MODE, N>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+  if (e != cudaSuccess) return e;
+  occ = max(1, occ);
+  int64_t grid = int64_t(L.num_sms) * occ;
+  if (grid > p.num_tiles) grid = p.num_tiles > 0 ? p.num_tiles : 1;
+  kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+
+template <int MODE, int LO, int HI>
+inline cudaError_t dispatch_range(const CoordLaunch& L, cudaStream_t stream) {
+  if constexpr (LO > HI) {
+    return cudaErrorInvalidValue;
+  } else {
+    if (L.R == LO) return launch_mode<MODE, LO>(L, stream);
+    return dispatch_range<MODE, LO + 1, HI>(L, stream);
+  }
+}
+
+}  // namespace gar

@@ -1,0 +1,319 @@
+// gar_api.cu — the C-ABI of libgar (include/gar.h): argument checks, workspace
+// carving and kernel sequencing.  No arithmetic of the method happens on the
+// host; every step runs in the kernels of coord_select*.cu, gram_*.cu and
+// select.cu.
+#include <cstdint>
+#include <cstring>
+#include <cuda_runtime.h>
+
+#include "../../include/gar.h"
+#include "common.cuh"
+#include "coord_select.h"
+#include "gram.h"
+
+namespace {
+
+using gar::CoordLaunch;
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+bool is_krum_family(gar_rule r) { return r == GAR_KRUM || r == GAR_MULTI_KRUM || r == GAR_BULYAN; }
+
+bool valid_rule(int r) { return r >= GAR_AVERAGE && r <= GAR_BULYAN; }
+
+// Effective m for (rule, n, f, m): Krum 1, Multi-Krum m (0 -> n-f-2).
+int effective_m(gar_rule rule, int n, int f, int m) {
+  if (rule == GAR_KRUM) return 1;
+  if (rule == GAR_MULTI_KRUM) return m == 0 ? n - f - 2 : m;
+  return 0;
+}
+
+// Pure argument checks (no CUDA calls): rule, sizes, quorum (PAPER.md l.208,
+// l.210-212, l.225), m.
+gar_status check_rule_args(gar_rule rule, int n, int f, int m) {
+  if (!valid_rule(rule) || n < 1 || n > GAR_MAX_N || f < 0) return GAR_ERR_INVALID_ARGUMENT;
+  switch (rule) {
+    case GAR_AVERAGE: return GAR_OK;
+    case GAR_MEDIAN:
+    case GAR_TRIMMED_MEAN: return n >= 2 * f + 1 ? GAR_OK : GAR_ERR_QUORUM;
+    case GAR_KRUM:
+    case GAR_MULTI_KRUM: {
+      if (n < 2 * f + 3) return GAR_ERR_QUORUM;
+      const int me = effective_m(rule, n, f, m);
+      if (m < 0 || me < 1 || me > n - f - 2) return GAR_ERR_INVALID_M;
+      return GAR_OK;
+    }
+    case GAR_BULYAN: return n >= 4 * f + 3 ? GAR_OK : GAR_ERR_QUORUM;
+  }
+  return GAR_ERR_INVALID_ARGUMENT;
+}
+
+gar_status check_rows(const float* const* grads, int n, int64_t d) {
+  if (!grads || d < 0) return GAR_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < n; ++i) {
+    if (!grads[i]) return GAR_ERR_INVALID_ARGUMENT;
+    if (reinterpret_cast<uintptr_t>(grads[i]) & 15u) return GAR_ERR_ALIGNMENT;
+  }
+  return GAR_OK;
+}
+
+gar_status check_out(const float* const* grads, int n, int64_t d, const float* out) {
+  if (!out) return GAR_ERR_INVALID_ARGUMENT;
+  if (reinterpret_cast<uintptr_t>(out) & 15u) return GAR_ERR_ALIGNMENT;
+  const uintptr_t o0 = reinterpret_cast<uintptr_t>(out), o1 = o0 + uintptr_t(d) * 4u;
+  for (int i = 0; i < n; ++i) {
+    const uintptr_t g0 = reinterpret_cast<uintptr_t>(grads[i]), g1 = g0 + uintptr_t(d) * 4u;
+    if (d > 0 && o0 < g1 && g0 < o1) return GAR_ERR_INVALID_ARGUMENT;
+  }
+  return GAR_OK;
+}
+
+// Device-pointer check (no CPU fallback: host memory is rejected).
+gar_status check_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return e == cudaErrorInvalidValue ? GAR_ERR_INVALID_ARGUMENT : GAR_ERR_CUDA;
+  }
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return GAR_ERR_INVALID_ARGUMENT;
+  return GAR_OK;
+}
+
+gar_status check_device_rows(const float* const* grads, int n, const void* out) {
+  for (int i = 0; i < n; ++i) {
+    gar_status s = check_device_ptr(grads[i]);
+    if (s != GAR_OK) return s;
+  }
+  return out ? check_device_ptr(out) : GAR_OK;
+}
+
+int num_sms() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+  return sms;
+}
+
+// Workspace layout (Krum family): [partials | G | idx], 256-byte aligned parts.
+struct Workspace {
+  double* partials;
+  double* G;
+  int32_t* idx;
+};
+
+size_t ws_bytes_for(int n) {
+  size_t b = align_up(sizeof(double) * gar::kGramMaxParts * n * n, 256);
+  b += align_up(sizeof(double) * n * n, 256);
+  b += align_up(sizeof(int32_t) * GAR_MAX_N, 256);
+  return b;
+}
+
+Workspace carve(void* ws, int n) {
+  unsigned char* p = static_cast<unsigned char*>(ws);
+  Workspace w;
+  w.partials = reinterpret_cast<double*>(p);
+  p += align_up(sizeof(double) * gar::kGramMaxParts * n * n, 256);
+  w.G = reinterpret_cast<double*>(p);
+  p += align_up(sizeof(double) * n * n, 256);
+  w.idx = reinterpret_cast<int32_t*>(p);
+  return w;
+}
+
+inline gar_status cuda_status(cudaError_t e) { return e == cudaSuccess ? GAR_OK : GAR_ERR_CUDA; }
+
+gar_status run_gram(const float* const* grads, int n, int64_t d, const Workspace& w, cudaStream_t st) {
+  int parts = 0;
+  cudaError_t e = gar::launch_gram_partials(grads, n, d, w.partials, num_sms(), &parts, st);
+  if (e != cudaSuccess) return GAR_ERR_CUDA;
+  return cuda_status(gar::launch_gram_reduce(w.partials, parts, n, w.G, st));
+}
+
+gar_status run_select(gar_rule rule, const double* G, int n, int f, int me, int32_t* idx, double* D_out,
+                      cudaStream_t st) {
+  const int srule = (rule == GAR_BULYAN) ? gar::kSelBulyan : gar::kSelMultiKrum;
+  return cuda_status(gar::launch_select(G, n, f, me, srule, idx, D_out, st));
+}
+
+gar_status run_combine(gar_rule rule, const float* const* grads, int n, int f, int me, int64_t d,
+                       const int32_t* idx, float* out, cudaStream_t st) {
+  CoordLaunch L{};
+  L.rows = grads;
+  L.n = n;
+  L.idx = idx;
+  L.f = f;
+  L.d = d;
+  L.out = out;
+  L.num_sms = num_sms();
+  if (rule == GAR_BULYAN) {
+    L.R = n - 2 * f;
+    return cuda_status(gar::launch_coord_select(gar::kModeBulyan, L, st));
+  }
+  L.R = me;
+  return cuda_status(gar::launch_coord_select(gar::kModeAverage, L, st));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gar_status_string(gar_status s) {
+  switch (s) {
+    case GAR_OK: return "GAR_OK";
+    case GAR_ERR_INVALID_ARGUMENT: return "GAR_ERR_INVALID_ARGUMENT";
+    case GAR_ERR_QUORUM: return "GAR_ERR_QUORUM";
+    case GAR_ERR_INVALID_M: return "GAR_ERR_INVALID_M";
+    case GAR_ERR_ALIGNMENT: return "GAR_ERR_ALIGNMENT";
+    case GAR_ERR_UNSUPPORTED: return "GAR_ERR_UNSUPPORTED";
+    case GAR_ERR_WORKSPACE: return "GAR_ERR_WORKSPACE";
+    case GAR_ERR_CUDA: return "GAR_ERR_CUDA";
+  }
+  return "GAR_ERR_UNKNOWN";
+}
+
+size_t gar_workspace_bytes(gar_rule rule, int n, int f, int64_t d) {
+  if (check_rule_args(rule, n, f, 0) != GAR_OK || d < 0) return 0;
+  if (!is_krum_family(rule)) return 0;
+  return ws_bytes_for(n);
+}
+
+int gar_num_selected(gar_rule rule, int n, int f, int m) {
+  if (check_rule_args(rule, n, f, m) != GAR_OK) return 0;
+  if (rule == GAR_BULYAN) return n - 2 * f;
+  return effective_m(rule, n, f, m);
+}
+
+gar_status gar_aggregate_ex(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d,
+                            float* out, int32_t* indices_dev, void* workspace, size_t workspace_bytes,
+                            gar_stream_t stream) {
+  gar_status s = check_rule_args(rule, n, f, m);
+  if (s != GAR_OK) return s;
+  if ((s = check_rows(grads, n, d)) != GAR_OK) return s;
+  if ((s = check_out(grads, n, d, out)) != GAR_OK) return s;
+  const bool krum = is_krum_family(rule);
+  if (krum && (!workspace || workspace_bytes < ws_bytes_for(n))) return GAR_ERR_WORKSPACE;
+  if ((s = check_device_rows(grads, n, out)) != GAR_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+
+  if (!krum) {
+    CoordLaunch L{};
+    L.rows = grads;
+    L.n = n;
+    L.idx = nullptr;
+    L.R = n;
+    L.f = f;
+    L.d = d;
+    L.out = out;
+    L.num_sms = num_sms();
+    int mode = gar::kModeAverage;
+    if (rule == GAR_MEDIAN) mode = gar::kModeMedian;
+    if (rule == GAR_TRIMMED_MEAN) mode = gar::kModeTrimmed;
+    return cuda_status(gar::launch_coord_select(mode, L, st));
+  }
+  const int me = effective_m(rule, n, f, m);
+  Workspace w = carve(workspace, n);
+  int32_t* idx = indices_dev ? indices_dev : w.idx;
+  if ((s = run_gram(grads, n, d, w, st)) != GAR_OK) return s;
+  if ((s = run_select(rule, w.G, n, f, me, idx, nullptr, st)) != GAR_OK) return s;
+  return run_combine(rule, grads, n, f, me, d, idx, out, st);
+}
+
+gar_status gar_aggregate(gar_rule rule, const float* const* grads, int n, int f, int64_t d, float* out,
+                         gar_stream_t stream) {
+  gar_status s = check_rule_args(rule, n, f, 0);
+  if (s != GAR_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  void* ws = nullptr;
+  const size_t bytes = gar_workspace_bytes(rule, n, f, d);
+  if (bytes) {
+    if (cudaMallocAsync(&ws, bytes, st) != cudaSuccess) return GAR_ERR_CUDA;
+  }
+  s = gar_aggregate_ex(rule, grads, n, f, 0, d, out, nullptr, ws, bytes, stream);
+  if (ws) {
+    if (cudaFreeAsync(ws, st) != cudaSuccess && s == GAR_OK) s = GAR_ERR_CUDA;
+  }
+  return s;
+}
+
+gar_status gar_select(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d,
+                      int32_t* indices_dev, int* n_selected_host, void* workspace, size_t workspace_bytes,
+                      gar_stream_t stream) {
+  gar_status s = check_rule_args(rule, n, f, m);
+  if (s != GAR_OK) return s;
+  if (!is_krum_family(rule)) return GAR_ERR_UNSUPPORTED;
+  if (!indices_dev) return GAR_ERR_INVALID_ARGUMENT;
+  if ((s = check_rows(grads, n, d)) != GAR_OK) return s;
+  if (!workspace || workspace_bytes < ws_bytes_for(n)) return GAR_ERR_WORKSPACE;
+  if ((s = check_device_rows(grads, n, nullptr)) != GAR_OK) return s;
+  if ((s = check_device_ptr(indices_dev)) != GAR_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int me = effective_m(rule, n, f, m);
+  Workspace w = carve(workspace, n);
+  if ((s = run_gram(grads, n, d, w, st)) != GAR_OK) return s;
+  if ((s = run_select(rule, w.G, n, f, me, indices_dev, nullptr, st)) != GAR_OK) return s;
+  if (n_selected_host) *n_selected_host = gar_num_selected(rule, n, f, m);
+  return GAR_OK;
+}
+
+gar_status gar_distances(const float* const* grads, int n, int64_t d, double* D_dev, void* workspace,
+                         size_t workspace_bytes, gar_stream_t stream) {
+  if (n < 1 || n > GAR_MAX_N || !D_dev) return GAR_ERR_INVALID_ARGUMENT;
+  gar_status s = check_rows(grads, n, d);
+  if (s != GAR_OK) return s;
+  if (!workspace || workspace_bytes < ws_bytes_for(n)) return GAR_ERR_WORKSPACE;
+  if ((s = check_device_rows(grads, n, nullptr)) != GAR_OK) return s;
+  if ((s = check_device_ptr(D_dev)) != GAR_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace w = carve(workspace, n);
+  if ((s = run_gram(grads, n, d, w, st)) != GAR_OK) return s;
+  return cuda_status(gar::launch_select(w.G, n, 0, 0, gar::kSelDistancesOnly, w.idx, D_dev, st));
+}
+
+gar_status gar_gram_partial(const float* const* grads, int n, int64_t d_local, double* gram_dev, void* workspace,
+                            size_t workspace_bytes, gar_stream_t stream) {
+  if (n < 1 || n > GAR_MAX_N || !gram_dev) return GAR_ERR_INVALID_ARGUMENT;
+  gar_status s = check_rows(grads, n, d_local);
+  if (s != GAR_OK) return s;
+  if (!workspace || workspace_bytes < ws_bytes_for(n)) return GAR_ERR_WORKSPACE;
+  if ((s = check_device_rows(grads, n, nullptr)) != GAR_OK) return s;
+  if ((s = check_device_ptr(gram_dev)) != GAR_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace w = carve(workspace, n);
+  int parts = 0;
+  if (gar::launch_gram_partials(grads, n, d_local, w.partials, num_sms(), &parts, st) != cudaSuccess)
+    return GAR_ERR_CUDA;
+  return cuda_status(gar::launch_gram_reduce(w.partials, parts, n, gram_dev, st));
+}
+
+gar_status gar_select_from_gram(gar_rule rule, const double* gram_dev, int n, int f, int m, int32_t* indices_dev,
+                                int* n_selected_host, void* workspace, size_t workspace_bytes,
+                                gar_stream_t stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  gar_status s = check_rule_args(rule, n, f, m);
+  if (s != GAR_OK) return s;
+  if (!is_krum_family(rule)) return GAR_ERR_UNSUPPORTED;
+  if (!gram_dev || !indices_dev) return GAR_ERR_INVALID_ARGUMENT;
+  if ((s = check_device_ptr(gram_dev)) != GAR_OK) return s;
+  if ((s = check_device_ptr(indices_dev)) != GAR_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int me = effective_m(rule, n, f, m);
+  if ((s = run_select(rule, gram_dev, n, f, me, indices_dev, nullptr, st)) != GAR_OK) return s;
+  if (n_selected_host) *n_selected_host = gar_num_selected(rule, n, f, m);
+  return GAR_OK;
+}
+
+gar_status gar_combine(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d_local,
+                       const int32_t* indices_dev, float* out, gar_stream_t stream) {
+  gar_status s = check_rule_args(rule, n, f, m);
+  if (s != GAR_OK) return s;
+  if (!is_krum_family(rule)) return GAR_ERR_UNSUPPORTED;
+  if (!indices_dev) return GAR_ERR_INVALID_ARGUMENT;
+  if ((s = check_rows(grads, n, d_local)) != GAR_OK) return s;
+  if ((s = check_out(grads, n, d_local, out)) != GAR_OK) return s;
+  if ((s = check_device_rows(grads, n, out)) != GAR_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return run_combine(rule, grads, n, f, effective_m(rule, n, f, m), d_local, indices_dev, out, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,205 @@
+#!/usr/bin/env python3
+"""Generate ``networks.cuh``: straight-line compare-exchange networks for the
+coordinate-selection kernel (product code; shares nothing with oracle/).
+
+For every size N in 1..64 we take Batcher's odd-even merge sort (and the
+bitonic sort) on the next power of two P >= N, with wires N..P-1 holding the
+constant +inf, constant-propagate the padding (a comparator against a +inf
+wire is a no-op or a relabel), then keep only the min/max outputs that reach
+the requested output positions.  The cheaper of the two constructions (in
+emitted min/max instructions) is kept per (N, outputs).
+
+Emitted functions (all in-place on ``float v[N]``, ascending order):
+
+* ``gar_net::sort_<N>(v)``    — full sort, every position valid;
+* ``gar_net::median_<N>(v)``  — only v[(N-1)/2] (and v[N/2] for even N) valid.
+
+Values must be canonical (no NaN, no -0): the kernel canonicalises first, so
+fminf/fmaxf (FMNMX) implement an exact compare-exchange.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+MAXN = 64
+
+
+def oddeven_merge_sort(P):
+    """Batcher's odd-even merge sort comparators for P = 2^k wires."""
+    comps = []
+
+    def merge(lo, n, r):
+        step = r * 2
+        if step < n:
+            merge(lo, n, step)
+            merge(lo + r, n, step)
+            for i in range(lo + r, lo + n - r, step):
+                comps.append((i, i + r))
+        else:
+            comps.append((lo, lo + r))
+
+    def sort(lo, n):
+        if n > 1:
+            m = n // 2
+            sort(lo, m)
+            sort(lo + m, m)
+            merge(lo, n, 1)
+
+    sort(0, P)
+    return comps
+
+
+def bitonic_sort(P):
+    comps = []
+    k = 2
+    while k <= P:
+        j = k // 2
+        while j > 0:
+            for i in range(P):
+                l = i ^ j
+                if l > i:
+                    if (i & k) == 0:
+                        comps.append((i, l))
+                    else:
+                        comps.append((l, i))   # descending block: min goes to l
+            j //= 2
+        k *= 2
+    return comps
+
+
+def build_ssa(N, comps):
+    """Symbolic execution.  Wire contents are ('in', i), ('inf',) or ('op', id).
+    Returns (ops, final) where ops[id] = (kind, a, b) with kind in {min,max}."""
+    P = 1
+    while P < N:
+        P *= 2
+    wires = [("in", i) if i < N else ("inf",) for i in range(P)]
+    ops = []
+    for (i, j) in comps:
+        a, b = wires[i], wires[j]
+        if a == ("inf",) and b == ("inf",):
+            continue
+        if b == ("inf",):
+            continue                      # min(a, inf) = a stays at i, inf at j
+        if a == ("inf",):
+            wires[i], wires[j] = b, a     # relabel
+            continue
+        ops.append(("min", a, b))
+        mn = ("op", len(ops) - 1)
+        ops.append(("max", a, b))
+        mx = ("op", len(ops) - 1)
+        wires[i], wires[j] = mn, mx
+    return ops, wires[:N]
+
+
+def live_ops(ops, outputs):
+    live = set()
+    stack = [o for o in outputs if o[0] == "op"]
+    while stack:
+        o = stack.pop()
+        if o[1] in live:
+            continue
+        live.add(o[1])
+        _, a, b = ops[o[1]]
+        for x in (a, b):
+            if x[0] == "op":
+                stack.append(x)
+    return live
+
+
+def best_network(N, positions):
+    P = 1
+    while P < N:
+        P *= 2
+    best = None
+    for name, comps in (("oddeven", oddeven_merge_sort(P)), ("bitonic", bitonic_sort(P))):
+        ops, final = build_ssa(N, comps)
+        live = live_ops(ops, [final[p] for p in positions])
+        cost = len(live)
+        if best is None or cost < best[0]:
+            best = (cost, name, ops, final, live)
+    return best
+
+
+def verify(N, ops, final, positions, trials=2000):
+    import random
+    rnd = random.Random(N)
+    for t in range(trials):
+        if N <= 12 and t < (1 << N):
+            vals = [(t >> i) & 1 for i in range(N)]          # 0-1 principle, exhaustive
+        else:
+            vals = [rnd.randint(-5, 5) for _ in range(N)]
+        res = {}
+
+        def ev(x):
+            if x[0] == "in":
+                return vals[x[1]]
+            if x[0] == "inf":
+                return float("inf")
+            if x[1] not in res:
+                k, a, b = ops[x[1]]
+                res[x[1]] = min(ev(a), ev(b)) if k == "min" else max(ev(a), ev(b))
+            return res[x[1]]
+
+        ref = sorted(vals)
+        for p in positions:
+            assert ev(final[p]) == ref[p], (N, p)
+
+
+def emit(N, fname, positions):
+    cost, name, ops, final, live = best_network(N, positions)
+    verify(N, ops, final, positions, trials=600 if N > 12 else (1 << N))
+    lines = [f"// N={N}: {name}, {cost} min/max ({'full sort' if len(positions) == N else 'median'})",
+             f"__device__ __forceinline__ void {fname}_{N}(float* v) {{"]
+    names = {}
+
+    def ref(x):
+        if x[0] == "in":
+            return f"v{x[1]}"
+        return names[x[1]]
+
+    for i in range(N):
+        lines.append(f"  const float v{i} = v[{i}];")
+    for k, (kind, a, b) in enumerate(ops):
+        if k not in live:
+            continue
+        nm = f"t{k}"
+        names[k] = nm
+        fn = "fminf" if kind == "min" else "fmaxf"
+        lines.append(f"  const float {nm} = {fn}({ref(a)}, {ref(b)});")
+    for p in positions:
+        lines.append(f"  v[{p}] = {ref(final[p])};")
+    lines.append("}")
+    return "\n".join(lines), cost
+
+
+def main(out_path):
+    parts = ["// GENERATED by gen_networks.py — do not edit.  Product code (libgar);",
+             "// shares nothing with oracle/.  Pruned Batcher / bitonic networks with",
+             "// +inf padding constant-propagated (DESIGN.md §5, coord_select).",
+             "#pragma once", "namespace gar_net {"]
+    table = []
+    for N in range(1, MAXN + 1):
+        src, c_sort = emit(N, "sort", list(range(N)))
+        parts.append(src)
+        med = [(N - 1) // 2] if N % 2 else [N // 2 - 1, N // 2]
+        src, c_med = emit(N, "median", med)
+        parts.append(src)
+        table.append((N, c_sort, c_med))
+    parts.append("template <int N> __device__ __forceinline__ void sort_net(float* v);")
+    parts.append("template <int N> __device__ __forceinline__ void median_net(float* v);")
+    for N in range(1, MAXN + 1):
+        parts.append(f"template <> __device__ __forceinline__ void sort_net<{N}>(float* v) {{ sort_{N}(v); }}")
+        parts.append(f"template <> __device__ __forceinline__ void median_net<{N}>(float* v) {{ median_{N}(v); }}")
+    parts.append("// min/max instruction counts (N, sort, median):")
+    for N, a, b in table:
+        parts.append(f"//   {N:2d} {a:4d} {b:4d}")
+    parts.append("}  // namespace gar_net")
+    with open(out_path, "w") as fh:
+        fh.write("\n".join(parts) + "\n")
+
+
+if __name__ == "__main__":
+    out = sys.argv[1] if len(sys.argv) > 1 else os.path.join(os.path.dirname(os.path.abspath(__file__)), "networks.cuh")
+    main(out)

@@ -1,0 +1,37 @@
+// gram.h — internal launch interface: Gram partials, their reduction, and the
+// selection kernel (rows a5-a7 of DESIGN.md §1).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gar {
+
+// Upper bound on the number of per-CTA partial Gram matrices (>= SM count).
+constexpr int kGramMaxParts = 160;
+
+// Per-coordinate centring reference c_k (DESIGN.md §4 "Gram"): the median of
+// fin(x_0k), fin(x_1k), fin(x_2k) (fin(v) = v if finite else 0), or fin(x_0k)
+// when n < 3.  A per-coordinate translation: D_ij is unchanged mathematically.
+
+// Partial Gram matrices of the centred rows, one fp64 [n x n] per CTA,
+// written to partials[p*n*n ...].  *n_parts receives the number written.
+cudaError_t launch_gram_partials(const float* const* rows, int n, int64_t d, double* partials,
+                                 int num_sms, int* n_parts, cudaStream_t stream);
+
+// Reference-quality SIMT Gram (fp64 products); test/debug only.
+cudaError_t launch_gram_partials_simt(const float* const* rows, int n, int64_t d, double* partials,
+                                      int num_sms, int* n_parts, cudaStream_t stream);
+
+// G = sum_p partials[p] in fixed order p = 0..n_parts-1 (deterministic).
+cudaError_t launch_gram_reduce(const double* partials, int n_parts, int n, double* G,
+                               cudaStream_t stream);
+
+enum SelectRule { kSelDistancesOnly = 0, kSelMultiKrum = 1, kSelBulyan = 2 };
+
+// From G: D (fp64 n x n, optional), then the selection of `rule`:
+// Multi-Krum -> m indices by ascending (score, index); Bulyan -> n-2f indices in
+// round order.  idx_out: device int32.
+cudaError_t launch_select(const double* G, int n, int f, int m, int rule, int32_t* idx_out,
+                          double* D_out, cudaStream_t stream);
+
+}  // namespace gar

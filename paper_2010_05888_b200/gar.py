@@ -1,0 +1,94 @@
+"""The paper's two-call interface, ``init(name, n, f)`` / ``aggregate(tensors)``
+(§4.1 "Aggregation"), over libgar.
+
+The Aggregator caches its device workspace (the paper's "allocating space only
+for one iteration along with the intermediate selected gradients", l.401:
+here one n x n Gram per CTA plus the selected indices).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+
+class Aggregator:
+    def __init__(self, rule: str, n: int, f: int, m: int | None = None):
+        self.rule = rule
+        self.rid = _lib.rule_id(rule)
+        self.n, self.f = int(n), int(f)
+        self.m = 0 if m is None else int(m)
+        # argument check (quorum, m) without touching the GPU
+        if rule in ("krum", "multi_krum", "bulyan"):
+            if _lib.gar_num_selected(rule, self.n, self.f, self.m) == 0:
+                raise _lib.GarError(2 if self.m == 0 else 3, f"init({rule!r}, n={n}, f={f}, m={m})")
+        elif _lib.gar_workspace_bytes(rule, self.n, self.f, 0) == 0 and not self._coord_ok():
+            raise _lib.GarError(2, f"init({rule!r}, n={n}, f={f})")
+        self._ws = {}
+        self._idx = {}
+
+    def _coord_ok(self):
+        if self.n < 1 or self.n > _lib.MAX_N or self.f < 0:
+            return False
+        if self.rule in ("median", "trimmed_mean"):
+            return self.n >= 2 * self.f + 1
+        return True
+
+    @property
+    def num_selected(self) -> int:
+        return _lib.gar_num_selected(self.rule, self.n, self.f, self.m)
+
+    def workspace(self, device) -> torch.Tensor | None:
+        nbytes = _lib.gar_workspace_bytes(self.rule, self.n, self.f, 0)
+        if nbytes == 0:
+            return None
+        key = str(device)
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            self._ws[key] = ws
+        return ws
+
+    def indices_buffer(self, device) -> torch.Tensor:
+        key = str(device)
+        t = self._idx.get(key)
+        if t is None:
+            t = torch.empty(_lib.MAX_N, dtype=torch.int32, device=device)
+            self._idx[key] = t
+        return t
+
+    def _check_n(self, grads):
+        n = grads.shape[0] if isinstance(grads, torch.Tensor) else len(grads)
+        if n != self.n:
+            raise ValueError(f"expected n = {self.n} gradients, got {n}")
+
+    def aggregate(self, grads, out: torch.Tensor | None = None, d: int | None = None,
+                  indices: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """out (fp32[d]) = GAR(grads); grads: list of n CUDA fp32 vectors or an [n, ld] matrix."""
+        self._check_n(grads)
+        arr, n, d, dev = _lib.row_pointers(grads, d)
+        if out is None:
+            out = torch.empty(d, dtype=torch.float32, device=dev)
+        ws = self.workspace(dev)
+        wsb = 0 if ws is None else ws.numel()
+        _lib.check(_lib.lib.gar_aggregate_ex(self.rid, arr, n, self.f, self.m, d, _lib._ptr(out),
+                                             _lib._ptr(indices), _lib._ptr(ws), wsb,
+                                             _lib.stream_handle(dev, stream)), f"aggregate[{self.rule}]")
+        return out
+
+    def select(self, grads, d: int | None = None, stream=None) -> torch.Tensor:
+        """Selected input indices (device int32), in selection order."""
+        self._check_n(grads)
+        arr, n, d, dev = _lib.row_pointers(grads, d)
+        ws = self.workspace(dev)
+        if ws is None:
+            raise _lib.GarError(5, f"select[{self.rule}]")
+        idx = torch.empty(_lib.MAX_N, dtype=torch.int32, device=dev)
+        nsel = _lib.gar_select(self.rule, grads, self.f, self.m, idx, ws, d=d, stream=stream)
+        return idx[:nsel]
+
+
+def init(name: str, n: int, f: int, m: int | None = None) -> Aggregator:
+    """"The init() function takes the name of the required GAR
+    (e.g., "median"), the value of n, the total number of inputs, and f"."""
+    return Aggregator(name, n, f, m)

@@ -1,0 +1,215 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bar (north_star): bit-exact for Median,
+trimmed mean, Average, the combine steps and selection indices (with the
+eps-tie rule for near-ties); distances within 1e-5 relative."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_helpers import (KRUM_FAMILY, assert_same_bits, check_selection, distances_close, to_device)
+
+pytestmark = pytest.mark.gpu
+
+RULES = ("average", "median", "trimmed_mean", "krum", "multi_krum", "bulyan")
+
+
+@pytest.fixture(scope="module")
+def gar():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2010_05888_b200 as g
+    return g
+
+
+def run_rule(gar, rule, X, d, f, m=None):
+    agg = gar.init(rule, X.shape[0], f, m)
+    idx = torch.full((64,), -1, dtype=torch.int32, device=X.device)
+    out = agg.aggregate(X, d=d, indices=idx if rule in KRUM_FAMILY else None)
+    torch.cuda.synchronize()
+    sel = idx[: agg.num_selected].cpu().numpy() if rule in KRUM_FAMILY else None
+    return out.cpu().numpy(), sel
+
+
+def check_rule(gar, rule, x, f, m=None, X=None):
+    n, d = x.shape
+    X = to_device(x) if X is None else X
+    out, sel = run_rule(gar, rule, X, d, f, m)
+    if rule == "average":
+        assert_same_bits(out, oracle.average(x), rule)
+    elif rule == "median":
+        assert_same_bits(out, oracle.median(x, f), rule)
+    elif rule == "trimmed_mean":
+        assert_same_bits(out, oracle.trimmed_mean(x, f), rule)
+    else:
+        D = oracle.distances(x)
+        mm = 1 if rule == "krum" else (n - f - 2 if m is None else m)
+        verdict = check_selection(rule, D, f, mm, sel)
+        if rule == "bulyan":
+            assert_same_bits(out, oracle.bulyan_coordinate_phase(x, f, sel), rule)
+        else:
+            assert_same_bits(out, oracle.mean_of_rows(x, sel), rule)
+        return verdict
+    return "exact"
+
+
+# ---------------------------------------------------------------- recipe inputs, several tiles + ragged tail
+@pytest.mark.parametrize("n,f,d", [(11, 2, synth.MNIST_CNN_D), (19, 4, 200_003), (31, 7, 300_001),
+                                   (7, 1, 4099), (63, 15, 40_005), (15, 3, 1)])
+@pytest.mark.parametrize("rule", RULES)
+def test_recipe_parity(gar, rule, n, f, d):
+    x = synth.make_gradients(n, f, d, seed=synth.BASE_SEED + n, ld=d).numpy()
+    check_rule(gar, rule, x, f)
+
+
+@pytest.mark.parametrize("n", list(range(1, 65)))
+def test_every_n_coordinatewise(gar, n):
+    """Every network size 1..64 (odd and even n), including ragged d."""
+    rng = np.random.default_rng(n)
+    d = 1000 + 3 * n + 1
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    x[:, :50] = rng.integers(-2, 3, (n, 50)).astype(np.float32)      # ties
+    f = (n - 1) // 2
+    check_rule(gar, "median", x, f)
+    check_rule(gar, "trimmed_mean", x, f // 2)
+    check_rule(gar, "average", x, 0)
+
+
+@pytest.mark.parametrize("n", [3, 5, 7, 8, 10, 11, 15, 19, 23, 31, 32, 33, 47, 63, 64])
+def test_every_family_size(gar, n):
+    f_b = (n - 3) // 4
+    x = synth.make_gradients(n, f_b, 3001, seed=77 + n, ld=3001).numpy()
+    check_rule(gar, "bulyan", x, f_b)
+    f_k = (n - 3) // 2
+    if f_k >= 0:
+        check_rule(gar, "krum", x, f_k)
+        check_rule(gar, "multi_krum", x, f_k)
+        check_rule(gar, "multi_krum", x, f_k, m=1)
+
+
+@pytest.mark.parametrize("theta,f", [(3, 0), (5, 1), (7, 1), (9, 2), (12, 3), (17, 7), (33, 15), (64, 0)])
+def test_bulyan_coordinate_phase_ties(gar, theta, f):
+    """Integer-valued rows force closeness ties between different values
+    (exercises the exact rank-count path); the selection is given explicitly
+    through gar_combine (n = theta + 2f rows)."""
+    n = theta + 2 * f
+    rng = np.random.default_rng(theta * 100 + f)
+    d = 2053
+    x = rng.integers(-4, 5, (n, d)).astype(np.float32)
+    x[:, ::7] = rng.standard_normal((n, len(range(0, d, 7)))).astype(np.float32)
+    sel = rng.permutation(n)[:theta].astype(np.int32)
+    out = torch.empty(d, dtype=torch.float32, device="cuda")
+    gar.gar_combine("bulyan", to_device(x), f, 0, torch.from_numpy(sel).cuda(), out, d=d)
+    torch.cuda.synchronize()
+    assert_same_bits(out.cpu().numpy(), oracle.bulyan_coordinate_phase(x, f, sel), "bulyan phase")
+
+
+def test_adversarial_values(gar):
+    """NaN / +-inf / -0 / 1e30 / denormals / duplicates / symmetric ties."""
+    for n, f in [(7, 1), (11, 2), (31, 7), (64, 15)]:
+        x = synth.adversarial_rows(n, 517, seed=n)
+        for rule in ("average", "median", "trimmed_mean"):
+            check_rule(gar, rule, x, f if rule != "average" else 0)
+        # Krum family: non-finite rows get +inf distances; compare the combine given the GPU selection
+        for rule in KRUM_FAMILY:
+            if rule == "bulyan" and n < 4 * f + 3:
+                continue
+            X = to_device(x)
+            out, sel = run_rule(gar, rule, X, x.shape[1], f)
+            if rule == "bulyan":
+                assert_same_bits(out, oracle.bulyan_coordinate_phase(x, f, sel), rule)
+            else:
+                assert_same_bits(out, oracle.mean_of_rows(x, sel), rule)
+
+
+def test_identical_inputs(gar):
+    v = np.random.default_rng(3).standard_normal(10_007).astype(np.float32)
+    for n in (7, 31, 63):
+        f = (n - 3) // 4
+        x = np.tile(v, (n, 1))
+        for rule in RULES:
+            out, _ = run_rule(gar, rule, to_device(x), x.shape[1], f)
+            assert_same_bits(out, v, rule)
+
+
+def test_distances_parity(gar):
+    for n, f, d in [(11, 2, synth.MNIST_CNN_D), (31, 7, 250_001), (64, 15, 30_000), (2, 0, 17)]:
+        x = synth.make_gradients(n, f, d, seed=5 + n, ld=d).numpy()
+        X = to_device(x)
+        ws = torch.empty(gar.gar_workspace_bytes("krum", max(n, 3), 0, d), dtype=torch.uint8, device="cuda")
+        D = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        gar.gar_distances(X, D, ws, d=d)
+        torch.cuda.synchronize()
+        distances_close(D.cpu().numpy(), oracle.distances(x))
+
+
+def test_distances_nonfinite(gar):
+    x = np.random.default_rng(0).standard_normal((9, 1000)).astype(np.float32)
+    x[3, 17] = np.nan
+    x[6, 500] = np.inf
+    ws = torch.empty(gar.gar_workspace_bytes("krum", 9, 0, 1000), dtype=torch.uint8, device="cuda")
+    D = torch.empty((9, 9), dtype=torch.float64, device="cuda")
+    gar.gar_distances(to_device(x), D, ws, d=1000)
+    D = D.cpu().numpy()
+    for r in (3, 6):
+        assert np.all(np.isinf(np.delete(D[r], r)))
+    distances_close(D, oracle.distances(x))
+
+
+def test_sharded_building_blocks_equal_whole(gar):
+    """gar_gram_partial over G coordinate slices, summed, then select + combine
+    per slice == the single-call result (the d-sharded path)."""
+    n, f, d = 31, 7, 100_000
+    x = synth.make_gradients(n, f, d, seed=99, ld=d).numpy()
+    X = to_device(x)
+    for rule in KRUM_FAMILY:
+        whole, sel = run_rule(gar, rule, X, d, f)
+        ws = torch.empty(gar.gar_workspace_bytes(rule, n, f, d), dtype=torch.uint8, device="cuda")
+        G = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+        bounds = [synth.shard_bounds(d, r, 4) for r in range(4)]
+        parts = []
+        for lo, hi in bounds:
+            Gp = torch.empty((n, n), dtype=torch.float64, device="cuda")
+            gar.gar_gram_partial([X[i, lo:hi] for i in range(n)], Gp, ws, d=hi - lo)
+            parts.append(Gp)
+        for Gp in parts:
+            G += Gp
+        idx = torch.empty(64, dtype=torch.int32, device="cuda")
+        k = gar.gar_select_from_gram(rule, G, n, f, 0, idx)
+        out = torch.empty(d, dtype=torch.float32, device="cuda")
+        for lo, hi in bounds:
+            gar.gar_combine(rule, [X[i, lo:hi] for i in range(n)], f, 0, idx, out[lo:hi], d=hi - lo)
+        torch.cuda.synchronize()
+        sel_sh = idx[:k].cpu().numpy()
+        D = oracle.distances(x)
+        mm = 1 if rule == "krum" else n - f - 2
+        check_selection(rule, D, f, mm, sel_sh)
+        if sel_sh.tolist() == sel.tolist():
+            assert_same_bits(out.cpu().numpy(), whole, rule)
+
+
+def test_determinism(gar):
+    x = synth.make_gradients(31, 7, 123_457, seed=4, ld=123_457).numpy()
+    X = to_device(x)
+    for rule in RULES:
+        a, sa = run_rule(gar, rule, X, x.shape[1], 7)
+        b, sb = run_rule(gar, rule, X, x.shape[1], 7)
+        assert_same_bits(a, b, rule)
+        if sa is not None:
+            assert sa.tolist() == sb.tolist()
+
+
+def test_errors_from_python(gar):
+    X = to_device(np.zeros((8, 16), np.float32))
+    with pytest.raises(gar.GarError):
+        gar.gar_aggregate_ex("median", X, 1, 0, X[0], d=16)               # out aliases row 0
+    host = torch.zeros(16)
+    with pytest.raises(gar.GarError) as e:
+        # host pointer for out: rejected (no CPU fallback)
+        import ctypes
+        from paper_2010_05888_b200 import _lib
+        arr, n, d, dev = _lib.row_pointers(X, 16)
+        _lib.check(_lib.lib.gar_aggregate_ex(1, arr, n, 1, 0, 16, ctypes.c_void_p(host.data_ptr()), None, None, 0,
+                                             None), "host out")
+    assert e.value.code == 1
