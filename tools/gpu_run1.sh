@@ -1,0 +1,9 @@
+cd $GRAFT_REPO_ROOT
+nvidia-smi -L > gpurun_out/r1_smi.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider > gpurun_out/r1_pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/r1_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r1_smoke.log 2>&1
+echo "smoke rc=$?" >> gpurun_out/r1_smoke.log
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/r1_bench.log 2>&1
+echo "bench rc=$?" >> gpurun_out/r1_bench.log
+tail -3 gpurun_out/r1_pytest_gpu.log gpurun_out/r1_smoke.log gpurun_out/r1_bench.log
