@@ -4,16 +4,19 @@
 // from which select.cu forms D_ij = G_ii + G_jj - 2 G_ij ("norm correction").
 //
 // Precision: h = x - c is split as h = hi + lo with
-// hi = rna_tf32(h) and lo = rna_tf32(h - hi); one tcgen05.mma kind::tf32 per
-// K-step multiplies A = [H; L] (M = 2*NP rows) by B = H (N = NP rows):
+// hi = h truncated to tf32 and lo = h - hi (exact); tcgen05.mma kind::tf32
+// multiplies A = [H; L] by B = H (M = 128, N = 64, block-diagonal packing of
+// two 64-coordinate blocks when n <= 32, see Cfg):
 //     D = [H H^T ; L H^T]   ->   G = H H^T + L H^T + (L H^T)^T
-// (3 of the 4 split products; the dropped lo*lo is < 2^-22 relative).  TMEM
+// (3 of the 4 split products; the dropped lo*lo is < 2^-20 relative).  TMEM
 // fp32 accumulators are drained every KT coordinates into fp64 registers.
 //
 // Warp roles (one persistent CTA per SM):
-//   7-8 warps   loaders: LDG.128 (streaming, evict-first) with a P-deep register
-//               prefetch ring, centring, hi/lo split, STS into the SWIZZLE_128B
-//               K-major operand layout, fence.proxy.async, mbarrier arrive;
+//   6-8 warps   loaders (warp = 16-coordinate slice of the tile, lane = 8 row
+//               groups x 4 chunks): LDG.128 streaming loads with a P-deep
+//               register prefetch ring, centring by warp shuffle, hi/lo split,
+//               STS into the
+//               SWIZZLE_128B K-major operand layout, fence.proxy.async, arrive;
 //   4 or 8 warps epilogue: tcgen05.ld of the accumulator lanes -> fp64 sums
 //               (8 when NP = 64: each thread owns half of a 64-column row);
 //   last warp   TMEM allocator + single-thread tcgen05.mma issuer.
@@ -30,28 +33,44 @@ namespace {
 template <int NP_>
 struct Cfg {
   static constexpr int NP = NP_;                 // padded row count (32 or 64)
-  static constexpr int M = 2 * NP;               // MMA M: H rows then L rows
-  static constexpr int N = NP;                   // MMA N: H rows
-  static constexpr int KT = 128;                 // coordinates per stage (tile)
-  static constexpr int ATOMS = KT / 32;          // 128-byte K atoms per stage
+  // Block-diagonal packing: a tile's coordinates are split into BLOCKS blocks
+  // that share the MMA's K index; A = [H_0..H_{B-1}; L_0..L_{B-1}] and
+  // B = [H_0..H_{B-1}], so the diagonal blocks of D = A B^T are the useful
+  // H_b H_b^T and L_b H_b^T (off-diagonal blocks pair different coordinates
+  // and are ignored).  NP = 32 -> 2 blocks, M = 128, N = 64: half the MMA
+  // instructions of M = 64, N = 32 and the full 128-lane datapath.
+  static constexpr int BLOCKS = 64 / NP;         // 2 / 1
+  static constexpr int M = 2 * NP * BLOCKS;      // 128: H rows of all blocks, then L rows
+  static constexpr int N = NP * BLOCKS;          // 64: H rows of all blocks
+  static constexpr int CONV_WARPS = (NP == 32) ? 8 : 6;   // converters: 16 coordinates each
+  static constexpr int KT = 16 * CONV_WARPS;     // coordinates per tile: 128 / 96
+  static constexpr int KB = KT / BLOCKS;         // coordinates per block (MMA K extent): 64 / 96
+  static constexpr int ATOMS = KB / 32;          // 128-byte K atoms per tile
   static constexpr int ATOM_BYTES = M * 128;     // one K atom of A (8-row groups of 1 KB)
-  static constexpr int STAGE_BYTES = ATOMS * ATOM_BYTES;
-  static constexpr int STAGES = (NP == 32) ? 4 : 3;
-  // Register budget: the CTA's warp count is rounded up to a multiple of 4 for
-  // register allocation, so 13 warps (NP = 32) and 16 warps (NP = 64) both
-  // leave 128 registers per thread.
-  static constexpr int LOADER_WARPS = (NP == 32) ? 8 : 7;
-  static constexpr int RPW = (NP + LOADER_WARPS - 1) / LOADER_WARPS;  // rows per loader warp (4 / 10)
-  static constexpr int PREFETCH = (NP == 32) ? 3 : 2;
-  static constexpr int EPI_WARP0 = LOADER_WARPS;
-  static constexpr int EPI_WARPS = (NP == 32) ? 4 : 8;    // 4 sub-partitions x column halves
-  static constexpr int EPI_COLS = N / (EPI_WARPS / 4);    // accumulator columns per epilogue thread
+  static constexpr int OP_BYTES = ATOMS * ATOM_BYTES;      // one operand stage (A; B aliases its H rows)
+  static constexpr int OP_STAGES = 2;
+  // Raw ring: one TMA bulk copy per row covers RAW_SUB tiles (2 KB / 768 B per
+  // row): the bulk-copy path is bound by requests, not bytes (tools/membench.cu).
+  static constexpr int RAW_SUB = (NP == 32) ? 4 : 2;
+  static constexpr int RAW_KT = RAW_SUB * KT;    // coordinates per raw stage
+  static constexpr int RAW_PITCH = RAW_KT * 4 + 16;   // bytes per raw row (+16: conflict-free LDS.128)
+  static constexpr int RAW_BYTES = NP * RAW_PITCH;    // one raw stage (TMA destination)
+  static constexpr int RAW_STAGES = 2;
+  // warp roles: converters | producer | epilogue | MMA.  The CTA's warp count is
+  // rounded up to a multiple of 4 for register allocation: 14 / 16 warps -> 128 regs.
+  static constexpr int PRODUCER_WARP = CONV_WARPS;
+  static constexpr int EPI_WARP0 = CONV_WARPS + 1;
+  static constexpr int EPI_WARPS = (NP == 32) ? 4 : 8;    // 4 sub-partitions (x column halves, NP = 64)
+  static constexpr int EPI_COLS = 32;                     // accumulator columns per epilogue thread
   static constexpr int MMA_WARP = EPI_WARP0 + EPI_WARPS;
   static constexpr int THREADS = (MMA_WARP + 1) * 32;
   static constexpr int TMEM_COLS = 2 * N;        // double-buffered accumulator
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 2 * KT * 4 /*c_buf*/ +
-                                    (2 * STAGES + 4) * 8 /*barriers*/ + 16;
-  static_assert(KT / 4 == 32, "one float4 chunk per lane per row");
+  static constexpr int SMEM_BYTES = OP_STAGES * OP_BYTES + RAW_STAGES * RAW_BYTES + 1024 /*align*/ +
+                                    (2 * OP_STAGES + 2 * RAW_STAGES + 4) * 8 /*barriers*/ + 16;
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  static_assert(2 * NP * (NP + 1) * 8 <= OP_STAGES * OP_BYTES, "epilogue T/B parking space");
+  static_assert(64 * 128 * 4 + 64 * 65 * 4 + 256 <= OP_STAGES * OP_BYTES, "centre-pick scratch");
+  static_assert(M == 128 && KB % 32 == 0, "tile shape");
 };
 
 // ---- tcgen05 / descriptor helpers ------------------------------------------
@@ -111,17 +130,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ float rna_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
+// hi part of the tf32 split: the top 11 significant bits (exact, one LOP3).
+// h - hi is then exact in fp32; the tensor core reads it as tf32 (keeping 11 of
+// its <= 13 significant bits), so each product is exact to ~2^-21 relative.
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 __device__ __forceinline__ float fin(float v) { return isfinite(v) ? v : 0.0f; }
-
-__device__ __forceinline__ float med3(float a, float b, float c) {
-  return fmaxf(fminf(a, b), fminf(fmaxf(a, b), c));
-}
 
 __device__ __forceinline__ void named_bar(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -141,74 +155,66 @@ __device__ __forceinline__ uint32_t sw128_offset(int row, int c16) {
   return static_cast<uint32_t>((row >> 3) * 1024 + (row & 7) * 128 + ((c16 ^ (row & 7)) << 4));
 }
 
-// Centre-row pick (runs on all threads of the CTA, uses `scratch` shared memory,
-// leaves the chosen row index in scratch[0] as an int).  Deterministic.
-template <class C>
-__device__ void center_pick(const RowPtrs& rows, int n, int64_t d, int64_t k_begin, unsigned char* scratch) {
-  constexpr int S = 256;                                   // sample coordinates
+// Centre-row pick, run by the converter warps (threads [0, NT), named barrier
+// 3) while the TMA producer already streams: the most central row of a
+// 128-coordinate sample of the CTA's slice, score_i = sum of the
+// floor((n-1)/2) smallest sample distances D_ij.  Deterministic.  `scratch`
+// (>= 49 KB of shared memory) is the idle operand ring.
+template <int NT>
+__device__ int center_pick(const RowPtrs& rows, int n, int64_t d, int64_t k_begin, unsigned char* scratch) {
+  constexpr int S = 128;                                   // sample coordinates
   float* xs = reinterpret_cast<float*>(scratch);           // [n][S]
   float* Ds = xs + GAR_MAX_N * S;                          // [64][65]
   float* score = Ds + GAR_MAX_N * (GAR_MAX_N + 1);         // [64]
-  if (n <= 2) {
-    __syncthreads();
-    if (threadIdx.x == 0) *reinterpret_cast<int*>(scratch) = 0;
-    __syncthreads();
-    return;
-  }
-  for (int e = threadIdx.x; e < n * (S / 4); e += C::THREADS) {
+  if (n <= 2) return 0;
+  const int t = threadIdx.x;
+  for (int e = t; e < n * (S / 4); e += NT) {
     const int r = e / (S / 4), q = e % (S / 4);
     const float4 v = load_chunk(rows.p[r], k_begin + 4 * q, d);
     reinterpret_cast<float4*>(xs + r * S)[q] = make_float4(fin(v.x), fin(v.y), fin(v.z), fin(v.w));
   }
-  __syncthreads();
+  named_bar(3, NT);
   const int np = n * (n - 1) / 2;
-  for (int p = threadIdx.x; p < np; p += C::THREADS) {
-    int i = 0, t = p;
-    while (t >= n - 1 - i) { t -= n - 1 - i; ++i; }
-    const int j = i + 1 + t;
+  for (int p = t; p < np; p += NT) {
+    int i = 0, u = p;
+    while (u >= n - 1 - i) { u -= n - 1 - i; ++i; }
+    const int j = i + 1 + u;
     const float4* a = reinterpret_cast<const float4*>(xs + i * S);
     const float4* b = reinterpret_cast<const float4*>(xs + j * S);
     float acc = 0.f;
     for (int k = 0; k < S / 4; ++k) {
-      const float4 u = a[k], v = b[k];
-      const float dx = u.x - v.x, dy = u.y - v.y, dz = u.z - v.z, dw = u.w - v.w;
+      const float4 x = a[k], y = b[k];
+      const float dx = x.x - y.x, dy = x.y - y.y, dz = x.z - y.z, dw = x.w - y.w;
       acc = fmaf(dx, dx, acc); acc = fmaf(dy, dy, acc); acc = fmaf(dz, dz, acc); acc = fmaf(dw, dw, acc);
     }
     if (!(acc <= 3.0e38f)) acc = __int_as_float(0x7f800000);
     Ds[i * (GAR_MAX_N + 1) + j] = acc;
     Ds[j * (GAR_MAX_N + 1) + i] = acc;
   }
-  __syncthreads();
+  named_bar(3, NT);
+  // score_i: sum (in j order) of the D_ij whose rank within row i (ties by j)
+  // is below h -- the h smallest
   const int h = (n - 1) / 2;
-  if (threadIdx.x < n) {
-    const int i = threadIdx.x;
-    // sum of the h smallest D_ij (j != i), ties by index, ascending order
-    float s = 0.f;
-    int last_j = -1;
-    float last_v = -1.f;
-    for (int t = 0; t < h; ++t) {
-      float bv = __int_as_float(0x7f800000);
-      int bj = -1;
-      for (int j = 0; j < n; ++j) {
-        if (j == i) continue;
-        const float v = Ds[i * (GAR_MAX_N + 1) + j];
-        const bool after = (v > last_v) || (v == last_v && j > last_j);
-        if (after && (bj < 0 || v < bv || (v == bv && j < bj))) { bv = v; bj = j; }
+  if (t < n) {
+    float sc = 0.f;
+    for (int j = 0; j < n; ++j) {
+      if (j == t) continue;
+      const float v = Ds[t * (GAR_MAX_N + 1) + j];
+      int rk = 0;
+      for (int k = 0; k < n; ++k) {
+        const float w = Ds[t * (GAR_MAX_N + 1) + k];
+        rk += (k != t && (w < v || (w == v && k < j))) ? 1 : 0;
       }
-      s += bv;
-      last_v = bv;
-      last_j = bj;
+      if (rk < h) sc += v;
     }
-    score[i] = s;
+    score[t] = sc;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int best = 0;
-    for (int i = 1; i < n; ++i)
-      if (score[i] < score[best]) best = i;
-    *reinterpret_cast<int*>(scratch) = best;
-  }
-  __syncthreads();
+  named_bar(3, NT);
+  int best = 0;
+  for (int i = 1; i < n; ++i)
+    if (score[i] < score[best]) best = i;
+  named_bar(3, NT);                                        // scratch is reused afterwards
+  return best;
 }
 
 template <int NP>
@@ -219,12 +225,15 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  unsigned char* stages = base;
-  float4* c_buf = reinterpret_cast<float4*>(base + C::STAGES * C::STAGE_BYTES);   // [2][32]
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + C::STAGES * C::STAGE_BYTES + 2 * C::KT * 4);
-  uint64_t* stage_free = full + C::STAGES;
-  uint64_t* acc_full = stage_free + C::STAGES;     // [2]
-  uint64_t* acc_empty = acc_full + 2;              // [2]
+  unsigned char* ops = base;                                        // OP_STAGES x A operand (SW128)
+  unsigned char* raw = base + C::OP_STAGES * C::OP_BYTES;           // RAW_STAGES x [NP][RAW_PITCH]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(raw + C::RAW_STAGES * C::RAW_BYTES);
+  uint64_t* raw_full = bars;                          // [RAW_STAGES] TMA bytes landed
+  uint64_t* raw_empty = raw_full + C::RAW_STAGES;     // [RAW_STAGES] converters done reading
+  uint64_t* op_full = raw_empty + C::RAW_STAGES;      // [OP_STAGES] operand written
+  uint64_t* op_free = op_full + C::OP_STAGES;         // [OP_STAGES] MMAs done reading
+  uint64_t* acc_full = op_free + C::OP_STAGES;        // [2]
+  uint64_t* acc_empty = acc_full + 2;                 // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -233,23 +242,14 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
   const int64_t t0 = num_tiles * blockIdx.x / G;
   const int64_t T = num_tiles * (blockIdx.x + 1) / G - t0;
 
-  // ---- centring row r* of this CTA: the most central row of a
-  // 256-coordinate sample of the CTA's own slice, score_i = sum of the
-  // floor((n-1)/2) smallest sample distances D_ij (a Krum score with the
-  // largest f any rule admits).  Per-coordinate centring is a translation, so
-  // each CTA may pick its own row.
-  __shared__ int center_row;
-  center_pick<C>(rows, n, d, t0 * C::KT, stages);
-  if (threadIdx.x == 0) center_row = *reinterpret_cast<int*>(stages);
-  __syncthreads();
-  const int rc = center_row;
-  // zero the operand ring once: rows >= n are never written afterwards
-  for (int i = threadIdx.x; i < C::STAGES * C::STAGE_BYTES / 16; i += C::THREADS)
-    reinterpret_cast<float4*>(stages)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], C::LOADER_WARPS);
-      mbar_init(&stage_free[s], 1);
+    for (int s = 0; s < C::RAW_STAGES; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], C::CONV_WARPS);
+    }
+    for (int s = 0; s < C::OP_STAGES; ++s) {
+      mbar_init(&op_full[s], C::CONV_WARPS);
+      mbar_init(&op_free[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -262,134 +262,167 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
                  "r"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp < C::LOADER_WARPS) {
-    // ====================================================== loaders
-    const int q = lane;                         // float4 chunk of the tile (coords 4q..4q+3)
-    const int atom = q >> 3, c16 = q & 7;
-    float4 ring[C::PREFETCH][C::RPW + 1];          // + the centre row (warp 0 only)
-    const float* crow = rows.p[rc];
+  if (warp == C::PRODUCER_WARP) {
+    // ====================================================== TMA producer
+    // One 1D bulk copy per row per raw stage (RAW_KT*4 bytes, 16-byte aligned,
+    // clamped to this CTA's range) into the raw ring, evict-first in L2.  Lane r
+    // issues row r (and r + 32).
+    const uint64_t pol = policy_evict_first();
+    const int64_t k_end = ((t0 + T) * C::KT < d) ? (t0 + T) * C::KT : d;
+    const int64_t R = (T + C::RAW_SUB - 1) / C::RAW_SUB;
+    for (int64_t j = 0; j < R; ++j) {
+      const int rs = static_cast<int>(j % C::RAW_STAGES);
+      const uint32_t use = static_cast<uint32_t>(j / C::RAW_STAGES);
+      if (use > 0) mbar_wait_sleep(&raw_empty[rs], (use - 1) & 1);
+      const int64_t k0 = t0 * C::KT + j * C::RAW_KT;
+      const int64_t cnt = (k_end - k0 < C::RAW_KT) ? k_end - k0 : C::RAW_KT;
+      const uint32_t bytes = static_cast<uint32_t>(cnt & ~int64_t(3)) * 4u;
+      if (lane == 0) mbar_arrive_expect_tx(&raw_full[rs], bytes * static_cast<uint32_t>(n));
+      __syncwarp();
+      if (bytes) {
+        unsigned char* dst = raw + rs * C::RAW_BYTES;
 #pragma unroll
-    for (int p = 0; p < C::PREFETCH; ++p) {
-      const int64_t k0 = (t0 + p) * C::KT + 4 * q;
-#pragma unroll
-      for (int j = 0; j < C::RPW; ++j) {
-        const int r = warp * C::RPW + j;
-        ring[p][j] = (p < T && r < n) ? load_chunk(rows.p[r], k0, d) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < NP / 32; ++u) {
+          const int r = lane + 32 * u;
+          if (r < n) bulk_g2s(dst + r * C::RAW_PITCH, rows.p[r] + k0, bytes, &raw_full[rs], pol);
+        }
       }
-      ring[p][C::RPW] = (p < T && warp == 0) ? load_chunk(crow, k0, d) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    for (int64_t i0 = 0; i0 < T; i0 += C::PREFETCH) {
+  } else if (warp < C::CONV_WARPS) {
+    // ====================================================== converters
+    // warp = 16-coordinate slice of the tile; lane = (chunk cq = lane/8, row
+    // group g = lane%8): rows g, g+8, ... of float4 chunk cq.  Raw rows are
+    // padded by 16 B so the 8-row LDS.128 phases are conflict-free; the SW128
+    // XOR swizzle does the same for the operand stores.
+    // ---- centring row r* of this CTA, picked while the
+    // producer's first raw stages are already in flight.  Per-coordinate
+    // centring is a translation, so each CTA may pick its own row.
+    constexpr int NT = C::CONV_WARPS * 32;
+    const int rc = center_pick<NT>(rows, n, d, t0 * C::KT, ops);
+    // zero the operand stages once: rows >= n are never written afterwards
+    for (int q = threadIdx.x; q < C::OP_STAGES * C::OP_BYTES / 16; q += NT)
+      reinterpret_cast<float4*>(ops)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    named_bar(3, NT);
+    constexpr int RR = NP / 8;                  // rows per lane
+    const int g = lane & 7, cq = lane >> 3;
+    const int Q = 4 * warp + cq;                // float4 chunk index within the tile
+    for (int64_t i = 0; i < T; ++i) {
+      const int64_t j = i / C::RAW_SUB;                   // raw stage index
+      const int sub = static_cast<int>(i % C::RAW_SUB);   // tile within the raw stage
+      const int rs = static_cast<int>(j % C::RAW_STAGES);
+      const int s = static_cast<int>(i % C::OP_STAGES);
+      if (sub == 0) mbar_wait(&raw_full[rs], static_cast<uint32_t>(j / C::RAW_STAGES) & 1);
+      const unsigned char* rt = raw + rs * C::RAW_BYTES + (sub * C::KT + 4 * Q) * 4;
+      // the tile holding coordinate d-1 may end in a (< 4-coordinate) chunk the
+      // bulk copy skipped; only that tile pays for 64-bit bounds checks
+      const bool last_tile = (t0 + i + 1) * C::KT > d;
+      const int64_t k0 = (t0 + i) * C::KT + 4 * Q;
+      const bool ragged = last_tile && (k0 + 4 > d);
+      float4 x[RR];
 #pragma unroll
-      for (int p = 0; p < C::PREFETCH; ++p) {
-        const int64_t i = i0 + p;
-        if (i >= T) break;
-        const int s = static_cast<int>(i % C::STAGES);
-        const uint32_t use = static_cast<uint32_t>(i / C::STAGES);
-        float4* x = ring[p];
-        // centring reference c_k = fin(x_{r*,k})
-        float4* cb = c_buf + (i & 1) * 32;
-        if (warp == 0) {
-          const float4 xc = x[C::RPW];
-          cb[q] = make_float4(fin(xc.x), fin(xc.y), fin(xc.z), fin(xc.w));
-        }
-        named_bar(1, C::LOADER_WARPS * 32);
-        const float4 c = cb[q];
-        if (use > 0) mbar_wait(&stage_free[s], (use - 1) & 1);
-        unsigned char* A = stages + s * C::STAGE_BYTES + atom * C::ATOM_BYTES;
-#pragma unroll
-        for (int j = 0; j < C::RPW; ++j) {
-          const int r = warp * C::RPW + j;
-          if (r < n) {
-            float4 h, hi, lo;
-            h.x = __fsub_rn(x[j].x, c.x); h.y = __fsub_rn(x[j].y, c.y);
-            h.z = __fsub_rn(x[j].z, c.z); h.w = __fsub_rn(x[j].w, c.w);
-            hi.x = rna_tf32(h.x); hi.y = rna_tf32(h.y); hi.z = rna_tf32(h.z); hi.w = rna_tf32(h.w);
-            lo.x = rna_tf32(__fsub_rn(h.x, hi.x)); lo.y = rna_tf32(__fsub_rn(h.y, hi.y));
-            lo.z = rna_tf32(__fsub_rn(h.z, hi.z)); lo.w = rna_tf32(__fsub_rn(h.w, hi.w));
-            *reinterpret_cast<float4*>(A + sw128_offset(r, c16)) = hi;
-            *reinterpret_cast<float4*>(A + sw128_offset(NP + r, c16)) = lo;
-          }
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[s]);
-        // refill this ring slot with tile i + PREFETCH
-        const int64_t k0 = (t0 + i + C::PREFETCH) * C::KT + 4 * q;
-        const bool more = i + C::PREFETCH < T;
-#pragma unroll
-        for (int j = 0; j < C::RPW; ++j) {
-          const int r = warp * C::RPW + j;
-          if (more && r < n) x[j] = load_chunk(rows.p[r], k0, d);
-        }
-        if (more && warp == 0) x[C::RPW] = load_chunk(crow, k0, d);
+      for (int u = 0; u < RR; ++u) {
+        const int r = g + 8 * u;
+        if (r < n) x[u] = ragged ? load_chunk(rows.p[r], k0, d) : *reinterpret_cast<const float4*>(rt + r * C::RAW_PITCH);
       }
+      float4 c = ragged ? load_chunk(rows.p[rc], k0, d) : *reinterpret_cast<const float4*>(rt + rc * C::RAW_PITCH);
+      c = make_float4(fin(c.x), fin(c.y), fin(c.z), fin(c.w));   // centring c_k = fin(x_{r*,k})
+      if (sub == C::RAW_SUB - 1 || i == T - 1) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&raw_empty[rs]);
+      }
+      if (i >= C::OP_STAGES) mbar_wait(&op_free[s], static_cast<uint32_t>(i / C::OP_STAGES - 1) & 1);
+      // chunk Q -> block b, chunk qb within the block's K range
+      constexpr int QB = C::KB / 4;                // float4 chunks per block
+      const int b = Q / QB, qb = Q % QB;
+      unsigned char* At = ops + s * C::OP_BYTES + (qb >> 3) * C::ATOM_BYTES;
+#pragma unroll
+      for (int u = 0; u < RR; ++u) {
+        const int r = g + 8 * u;
+        if (r < n) {
+          float4 h, hi, lo;
+          h.x = __fsub_rn(x[u].x, c.x); h.y = __fsub_rn(x[u].y, c.y);
+          h.z = __fsub_rn(x[u].z, c.z); h.w = __fsub_rn(x[u].w, c.w);
+          hi.x = tf32_trunc(h.x); hi.y = tf32_trunc(h.y); hi.z = tf32_trunc(h.z); hi.w = tf32_trunc(h.w);
+          lo.x = __fsub_rn(h.x, hi.x); lo.y = __fsub_rn(h.y, hi.y);
+          lo.z = __fsub_rn(h.z, hi.z); lo.w = __fsub_rn(h.w, hi.w);
+          *reinterpret_cast<float4*>(At + sw128_offset(b * NP + r, qb & 7)) = hi;
+          *reinterpret_cast<float4*>(At + sw128_offset(C::N + b * NP + r, qb & 7)) = lo;
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&op_full[s]);
     }
   } else if (warp == C::MMA_WARP) {
     // ====================================================== MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = tf32_idesc<C::M, C::N>();
-      const uint32_t stage0 = smem_u32(stages);
+      const uint32_t op0 = smem_u32(ops);
       for (int64_t i = 0; i < T; ++i) {
-        const int s = static_cast<int>(i % C::STAGES);
+        const int s = static_cast<int>(i % C::OP_STAGES);
         const int buf = static_cast<int>(i & 1);
         const uint32_t nb = static_cast<uint32_t>(i >> 1);
-        if (nb > 0) mbar_wait(&acc_empty[buf], (nb - 1) & 1);
-        mbar_wait(&full[s], static_cast<uint32_t>(i / C::STAGES) & 1);
+        if (nb > 0) mbar_wait_sleep(&acc_empty[buf], (nb - 1) & 1);
+        mbar_wait_sleep(&op_full[s], static_cast<uint32_t>(i / C::OP_STAGES) & 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * C::N;
 #pragma unroll
-        for (int kk = 0; kk < C::KT / 8; ++kk) {
-          const uint32_t a = stage0 + s * C::STAGE_BYTES + (kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32;
+        for (int kk = 0; kk < C::KB / 8; ++kk) {
+          const uint32_t a = op0 + s * C::OP_BYTES + (kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32;
           const uint64_t desc = sw128_desc(a);
           mma_tf32(d_tmem, desc, desc, idesc, kk > 0 ? 1u : 0u);
         }
-        mma_commit(&stage_free[s]);
+        mma_commit(&op_free[s]);
         mma_commit(&acc_full[buf]);
       }
     }
     __syncwarp();
   } else {
     // ====================================================== epilogue (TMEM -> fp64)
+    // Warp -> TMEM sub-partition e (D rows m = 32e + lane).  Rows [0, N) are
+    // H_b rows, [N, 2N) L_b rows, b = (m mod N) / NP; the useful columns of
+    // block b are [b*NP, (b+1)*NP).  NP = 64: two warps per sub-partition,
+    // one per 32-column half.
     const int ew = warp - C::EPI_WARP0;
-    const int e = warp & 3;                      // TMEM sub-partition of this warp
-    const int col0 = (ew >> 2) * C::EPI_COLS;    // column half (NP = 64) or 0
+    const int e = warp & 3;
+    const int m = 32 * e + lane;
+    const int blk = (m % C::N) / NP;
+    const int col0 = (C::BLOCKS > 1) ? blk * NP : (ew >> 2) * 32;
     double acc[C::EPI_COLS];
 #pragma unroll
     for (int j = 0; j < C::EPI_COLS; ++j) acc[j] = 0.0;
     for (int64_t i = 0; i < T; ++i) {
       const int buf = static_cast<int>(i & 1);
-      mbar_wait(&acc_full[buf], static_cast<uint32_t>(i >> 1) & 1);
+      mbar_wait_sleep(&acc_full[buf], static_cast<uint32_t>(i >> 1) & 1);
       tc_fence_after();
       float v[C::EPI_COLS];
-#pragma unroll
-      for (int h = 0; h < C::EPI_COLS / 32; ++h)
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * e) << 16) + buf * C::N + col0 + 32 * h, v + 32 * h);
+      tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * e) << 16) + buf * C::N + col0, v);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
 #pragma unroll
       for (int j = 0; j < C::EPI_COLS; ++j) acc[j] += static_cast<double>(v[j]);
     }
-    // D row held by this thread: M=64 -> lanes 0-15 of each sub-partition; M=128 -> all lanes
-    int m = -1;
-    if (C::M == 64) {
-      if (lane < 16) m = 16 * e + lane;
-    } else {
-      m = 32 * e + lane;
-    }
-    // park T = H H^T (rows 0..NP-1) and B = L H^T (rows NP..2NP-1) in shared memory
+    // park T = sum_b H_b H_b^T (TB rows 0..NP-1) and B = sum_b L_b H_b^T
+    // (rows NP..2NP-1) in shared memory; blocks are added in fixed order b = 0, 1
     constexpr int EPI_THREADS = C::EPI_WARPS * 32;
-    double* TB = reinterpret_cast<double*>(stages);       // [2NP][NP+1]; operand ring is idle now
+    double* TB = reinterpret_cast<double*>(ops);          // [2NP][NP+1]; operand stages are idle now
+    const int tb_row = (m < C::N ? 0 : NP) + (m % NP);
+    const int tb_col = (C::BLOCKS > 1) ? 0 : col0;
     named_bar(2, EPI_THREADS);
-    if (m >= 0) {
+    if (blk == 0) {
 #pragma unroll
-      for (int j = 0; j < C::EPI_COLS; ++j) TB[m * (NP + 1) + col0 + j] = acc[j];
+      for (int j = 0; j < C::EPI_COLS; ++j) TB[tb_row * (NP + 1) + tb_col + j] = acc[j];
+    }
+    named_bar(2, EPI_THREADS);
+    if (blk == 1) {
+#pragma unroll
+      for (int j = 0; j < C::EPI_COLS; ++j) TB[tb_row * (NP + 1) + tb_col + j] += acc[j];
     }
     named_bar(2, EPI_THREADS);
     double* P = partials + static_cast<size_t>(blockIdx.x) * n * n;
