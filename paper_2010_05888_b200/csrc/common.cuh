@@ -34,34 +34,23 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Wait for the phase with parity `parity` to complete.  try_wait with a
+// suspend-time hint parks the thread in hardware until the phase completes (or
+// the hint expires), so waiting warps do not steal issue slots by polling.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n}" ::"r"(addr),
-      "r"(parity)
+      "r"(parity), "r"(1000000u)
       : "memory");
 }
 
-// Same, with a short sleep between polls: for waiters whose wake-up latency is
-// hidden (double-buffered consumers), so spinning does not steal issue slots.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
-  uint32_t done;
-  while (true) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n\t}"
-        : "=r"(done)
-        : "r"(addr), "r"(parity)
-        : "memory");
-    if (done) return;
-    __nanosleep(64);
-  }
-}
+// Same wait, for latency-tolerant waiters (kept as a separate name so the
+// policy can differ per role).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
 
 // 1D bulk async copy global -> shared (TMA engine), completes on an mbarrier.
 // dst, src, bytes must be 16-byte aligned / a multiple of 16.

@@ -9,7 +9,7 @@
 // two 64-coordinate blocks when n <= 32, see Cfg):
 //     D = [H H^T ; L H^T]   ->   G = H H^T + L H^T + (L H^T)^T
 // (3 of the 4 split products; the dropped lo*lo is < 2^-20 relative).  TMEM
-// fp32 accumulators are drained every KT coordinates into fp64 registers.
+// fp32 accumulators are drained every FLUSH tiles into fp64 registers.
 //
 // Warp roles (one persistent CTA per SM):
 //   6-8 warps   loaders (warp = 16-coordinate slice of the tile, lane = 8 row
@@ -65,6 +65,7 @@ struct Cfg {
   static constexpr int MMA_WARP = EPI_WARP0 + EPI_WARPS;
   static constexpr int THREADS = (MMA_WARP + 1) * 32;
   static constexpr int TMEM_COLS = 2 * N;        // double-buffered accumulator
+  static constexpr int FLUSH = 2;                // tiles accumulated in TMEM (fp32) per fp64 drain
   static constexpr int SMEM_BYTES = OP_STAGES * OP_BYTES + RAW_STAGES * RAW_BYTES + 1024 /*align*/ +
                                     (2 * OP_STAGES + 2 * RAW_STAGES + 4) * 8 /*barriers*/ + 16;
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
@@ -223,8 +224,9 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
                    double* __restrict__ partials) {
   using C = Cfg<NP>;
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // 1024-byte alignment (SWIZZLE_128B) by offsetting the shared array itself, so
+  // the compiler keeps the shared address space (LDS/STS, not generic LD/ST)
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* ops = base;                                        // OP_STAGES x A operand (SW128)
   unsigned char* raw = base + C::OP_STAGES * C::OP_BYTES;           // RAW_STAGES x [NP][RAW_PITCH]
   uint64_t* bars = reinterpret_cast<uint64_t*>(raw + C::RAW_STAGES * C::RAW_BYTES);
@@ -311,52 +313,72 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
     constexpr int RR = NP / 8;                  // rows per lane
     const int g = lane & 7, cq = lane >> 3;
     const int Q = 4 * warp + cq;                // float4 chunk index within the tile
-    for (int64_t i = 0; i < T; ++i) {
-      const int64_t j = i / C::RAW_SUB;                   // raw stage index
-      const int sub = static_cast<int>(i % C::RAW_SUB);   // tile within the raw stage
+    // chunk Q -> block b, chunk qb within the block's K range
+    constexpr int QB = C::KB / 4;               // float4 chunks per block
+    const int b = Q / QB, qb = Q % QB;
+    // per-lane constant shared-memory offsets
+    const unsigned char* raw_me = raw + Q * 16 + g * C::RAW_PITCH;
+    const unsigned char* raw_c = raw + Q * 16 + rc * C::RAW_PITCH;
+    uint32_t off_hi[RR], off_lo[RR];
+#pragma unroll
+    for (int u = 0; u < RR; ++u) {
+      const int r = g + 8 * u;
+      off_hi[u] = (qb >> 3) * C::ATOM_BYTES + sw128_offset(b * NP + r, qb & 7);
+      off_lo[u] = (qb >> 3) * C::ATOM_BYTES + sw128_offset(C::N + b * NP + r, qb & 7);
+    }
+    static_assert(C::RAW_SUB % C::OP_STAGES == 0, "operand stage = sub % OP_STAGES");
+    const int64_t R = (T + C::RAW_SUB - 1) / C::RAW_SUB;
+    for (int64_t j = 0; j < R; ++j) {
       const int rs = static_cast<int>(j % C::RAW_STAGES);
-      const int s = static_cast<int>(i % C::OP_STAGES);
-      if (sub == 0) mbar_wait(&raw_full[rs], static_cast<uint32_t>(j / C::RAW_STAGES) & 1);
-      const unsigned char* rt = raw + rs * C::RAW_BYTES + (sub * C::KT + 4 * Q) * 4;
-      // the tile holding coordinate d-1 may end in a (< 4-coordinate) chunk the
-      // bulk copy skipped; only that tile pays for 64-bit bounds checks
-      const bool last_tile = (t0 + i + 1) * C::KT > d;
-      const int64_t k0 = (t0 + i) * C::KT + 4 * Q;
-      const bool ragged = last_tile && (k0 + 4 > d);
-      float4 x[RR];
+      mbar_wait(&raw_full[rs], static_cast<uint32_t>(j / C::RAW_STAGES) & 1);
 #pragma unroll
-      for (int u = 0; u < RR; ++u) {
-        const int r = g + 8 * u;
-        if (r < n) x[u] = ragged ? load_chunk(rows.p[r], k0, d) : *reinterpret_cast<const float4*>(rt + r * C::RAW_PITCH);
-      }
-      float4 c = ragged ? load_chunk(rows.p[rc], k0, d) : *reinterpret_cast<const float4*>(rt + rc * C::RAW_PITCH);
-      c = make_float4(fin(c.x), fin(c.y), fin(c.z), fin(c.w));   // centring c_k = fin(x_{r*,k})
-      if (sub == C::RAW_SUB - 1 || i == T - 1) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&raw_empty[rs]);
-      }
-      if (i >= C::OP_STAGES) mbar_wait(&op_free[s], static_cast<uint32_t>(i / C::OP_STAGES - 1) & 1);
-      // chunk Q -> block b, chunk qb within the block's K range
-      constexpr int QB = C::KB / 4;                // float4 chunks per block
-      const int b = Q / QB, qb = Q % QB;
-      unsigned char* At = ops + s * C::OP_BYTES + (qb >> 3) * C::ATOM_BYTES;
+      for (int sub = 0; sub < C::RAW_SUB; ++sub) {
+        const int64_t i = j * C::RAW_SUB + sub;
+        if (i >= T) break;
+        const int s = sub % C::OP_STAGES;
+        const unsigned char* rt = raw_me + rs * C::RAW_BYTES + sub * C::KT * 4;
+        const unsigned char* rtc = raw_c + rs * C::RAW_BYTES + sub * C::KT * 4;
+        // the tile holding coordinate d-1 may end in a (< 4-coordinate) chunk the
+        // bulk copy skipped; only that tile pays for 64-bit bounds checks
+        const bool last_tile = (t0 + i + 1) * C::KT > d;
+        float4 x[RR], c;
+        if (!last_tile) {
 #pragma unroll
-      for (int u = 0; u < RR; ++u) {
-        const int r = g + 8 * u;
-        if (r < n) {
-          float4 h, hi, lo;
-          h.x = __fsub_rn(x[u].x, c.x); h.y = __fsub_rn(x[u].y, c.y);
-          h.z = __fsub_rn(x[u].z, c.z); h.w = __fsub_rn(x[u].w, c.w);
-          hi.x = tf32_trunc(h.x); hi.y = tf32_trunc(h.y); hi.z = tf32_trunc(h.z); hi.w = tf32_trunc(h.w);
-          lo.x = __fsub_rn(h.x, hi.x); lo.y = __fsub_rn(h.y, hi.y);
-          lo.z = __fsub_rn(h.z, hi.z); lo.w = __fsub_rn(h.w, hi.w);
-          *reinterpret_cast<float4*>(At + sw128_offset(b * NP + r, qb & 7)) = hi;
-          *reinterpret_cast<float4*>(At + sw128_offset(C::N + b * NP + r, qb & 7)) = lo;
+          for (int u = 0; u < RR; ++u)
+            if (g + 8 * u < n) x[u] = *reinterpret_cast<const float4*>(rt + u * 8 * C::RAW_PITCH);
+          c = *reinterpret_cast<const float4*>(rtc);
+        } else {
+          const int64_t k0 = (t0 + i) * C::KT + 4 * Q;
+          const bool ragged = k0 + 4 > d;
+#pragma unroll
+          for (int u = 0; u < RR; ++u) {
+            const int r = g + 8 * u;
+            if (r < n) x[u] = ragged ? load_chunk(rows.p[r], k0, d) : *reinterpret_cast<const float4*>(rt + u * 8 * C::RAW_PITCH);
+          }
+          c = ragged ? load_chunk(rows.p[rc], k0, d) : *reinterpret_cast<const float4*>(rtc);
         }
+        c = make_float4(fin(c.x), fin(c.y), fin(c.z), fin(c.w));   // centring c_k = fin(x_{r*,k})
+        if (i >= C::OP_STAGES) mbar_wait(&op_free[s], static_cast<uint32_t>(i / C::OP_STAGES - 1) & 1);
+        unsigned char* At = ops + s * C::OP_BYTES;
+#pragma unroll
+        for (int u = 0; u < RR; ++u) {
+          if (g + 8 * u < n) {
+            float4 h, hi, lo;
+            h.x = __fsub_rn(x[u].x, c.x); h.y = __fsub_rn(x[u].y, c.y);
+            h.z = __fsub_rn(x[u].z, c.z); h.w = __fsub_rn(x[u].w, c.w);
+            hi.x = tf32_trunc(h.x); hi.y = tf32_trunc(h.y); hi.z = tf32_trunc(h.z); hi.w = tf32_trunc(h.w);
+            lo.x = __fsub_rn(h.x, hi.x); lo.y = __fsub_rn(h.y, hi.y);
+            lo.z = __fsub_rn(h.z, hi.z); lo.w = __fsub_rn(h.w, hi.w);
+            *reinterpret_cast<float4*>(At + off_hi[u]) = hi;
+            *reinterpret_cast<float4*>(At + off_lo[u]) = lo;
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&op_full[s]);
       }
-      fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&op_full[s]);
+      if (lane == 0) mbar_arrive(&raw_empty[rs]);
     }
   } else if (warp == C::MMA_WARP) {
     // ====================================================== MMA issuer
@@ -365,9 +387,11 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
       const uint32_t op0 = smem_u32(ops);
       for (int64_t i = 0; i < T; ++i) {
         const int s = static_cast<int>(i % C::OP_STAGES);
-        const int buf = static_cast<int>(i & 1);
-        const uint32_t nb = static_cast<uint32_t>(i >> 1);
-        if (nb > 0) mbar_wait_sleep(&acc_empty[buf], (nb - 1) & 1);
+        const int64_t chunk = i / C::FLUSH;                 // accumulation chunk
+        const int buf = static_cast<int>(chunk & 1);
+        const bool first = (i % C::FLUSH) == 0;
+        const bool last = (i % C::FLUSH) == C::FLUSH - 1 || i == T - 1;
+        if (first && chunk >= 2) mbar_wait_sleep(&acc_empty[buf], static_cast<uint32_t>((chunk >> 1) - 1) & 1);
         mbar_wait_sleep(&op_full[s], static_cast<uint32_t>(i / C::OP_STAGES) & 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * C::N;
@@ -375,10 +399,10 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
         for (int kk = 0; kk < C::KB / 8; ++kk) {
           const uint32_t a = op0 + s * C::OP_BYTES + (kk >> 2) * C::ATOM_BYTES + (kk & 3) * 32;
           const uint64_t desc = sw128_desc(a);
-          mma_tf32(d_tmem, desc, desc, idesc, kk > 0 ? 1u : 0u);
+          mma_tf32(d_tmem, desc, desc, idesc, (first && kk == 0) ? 0u : 1u);
         }
         mma_commit(&op_free[s]);
-        mma_commit(&acc_full[buf]);
+        if (last) mma_commit(&acc_full[buf]);
       }
     }
     __syncwarp();
@@ -396,7 +420,8 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
     double acc[C::EPI_COLS];
 #pragma unroll
     for (int j = 0; j < C::EPI_COLS; ++j) acc[j] = 0.0;
-    for (int64_t i = 0; i < T; ++i) {
+    const int64_t nchunks = (T + C::FLUSH - 1) / C::FLUSH;
+    for (int64_t i = 0; i < nchunks; ++i) {
       const int buf = static_cast<int>(i & 1);
       mbar_wait_sleep(&acc_full[buf], static_cast<uint32_t>(i >> 1) & 1);
       tc_fence_after();
