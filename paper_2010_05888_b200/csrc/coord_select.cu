@@ -21,7 +21,10 @@ cudaError_t launch_coord_bulyan_49_64(const CoordLaunch& L, cudaStream_t stream)
 cudaError_t launch_coord_select(int mode, const CoordLaunch& L, cudaStream_t stream) {
   if (L.d == 0) return cudaSuccess;
   if (L.R < 1 || L.R > GAR_MAX_N) return cudaErrorInvalidValue;
-  if (mode == kModeAverage) return launch_mode<kModeAverage, 0>(L, stream);
+  if (mode == kModeAverage) {
+    if (L.R == 1) return launch_copy_row(L, stream);
+    return launch_mode<kModeAverage, 0>(L, stream);
+  }
   const int band = (L.R - 1) / 16;
   switch (mode) {
     case kModeMedian:

@@ -23,9 +23,13 @@
 
 namespace gar {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kTile = kConsumerWarps * 32;       // coordinates per tile
-constexpr int kThreads = kTile + 32;             // + 1 producer warp
+// W consumer warps (one coordinate per thread per tile) + 1 producer warp.
+// W = 15 for up to 32 rows: 480-coordinate tiles = 1920 B per row per bulk
+// copy, 16 warps per CTA (128 registers), one CTA per SM with a ~180 KB ring;
+// W = 7 above 32 rows keeps 3 stages of 63 rows in shared memory.  Large
+// copies matter: the bulk-copy path is bound by requests (tools/membench.cu).
+template <int N>
+constexpr int consumer_warps() { return N <= 32 ? 15 : 7; }
 
 struct CoordParams {
   RowPtrs rows;
@@ -130,8 +134,10 @@ __device__ __forceinline__ float bulyan_column(float* v, float* col, int stride,
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int MODE, int N>
-__global__ void __launch_bounds__(kThreads, 2) coord_select_kernel(const __grid_constant__ CoordParams p) {
+template <int MODE, int N, int W>
+__global__ void __launch_bounds__(32 * (W + 1), 1) coord_select_kernel(const __grid_constant__ CoordParams p) {
+  constexpr int kConsumerWarps = W;
+  constexpr int kTile = 32 * W;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int R = (N > 0) ? N : p.R;
   const int stages = p.stages;
@@ -223,9 +229,37 @@ __global__ void __launch_bounds__(kThreads, 2) coord_select_kernel(const __grid_
   }
 }
 
+// Krum combine (one selected row): out = fp32((0 + x) / 1) = x + 0 (-0 -> +0),
+// a plain vectorised streaming copy.
+__global__ void __launch_bounds__(256) copy_row_kernel(const __grid_constant__ RowPtrs rows, const int32_t* idx,
+                                                        float* __restrict__ out, int64_t d) {
+  const float* src = rows.p[idx ? idx[0] : 0];
+  const int64_t n4 = d >> 2;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n4; q += int64_t(gridDim.x) * blockDim.x) {
+    float4 v = __ldcs(reinterpret_cast<const float4*>(src) + q);
+    v.x = __fadd_rn(v.x, 0.0f); v.y = __fadd_rn(v.y, 0.0f); v.z = __fadd_rn(v.z, 0.0f); v.w = __fadd_rn(v.w, 0.0f);
+    __stcs(reinterpret_cast<float4*>(out) + q, v);
+  }
+  const int64_t k = (n4 << 2) + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (blockIdx.x == 0 && k < d) out[k] = __fadd_rn(src[k], 0.0f);
+}
+
+inline cudaError_t launch_copy_row(const CoordLaunch& L, cudaStream_t stream) {
+  RowPtrs rp;
+  for (int i = 0; i < GAR_MAX_N; ++i) rp.p[i] = (i < L.n) ? L.rows[i] : nullptr;
+  int64_t blocks = (L.d / 4 + 255) / 256;
+  const int64_t cap = int64_t(L.num_sms) * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  copy_row_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(rp, L.idx, L.out, L.d);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- host side
-template <int MODE, int N>
-inline cudaError_t launch_mode(const CoordLaunch& L, cudaStream_t stream) {
+template <int MODE, int N, int W>
+inline cudaError_t launch_mode_w(const CoordLaunch& L, cudaStream_t stream) {
+  constexpr int kTile = 32 * W;
+  constexpr int kThreads = 32 * (W + 1);
   CoordParams p;
   for (int i = 0; i < GAR_MAX_N; ++i) p.rows.p[i] = (i < L.n) ? L.rows[i] : nullptr;
   p.idx = L.idx;
@@ -234,12 +268,12 @@ inline cudaError_t launch_mode(const CoordLaunch& L, cudaStream_t stream) {
   p.R = L.R;
   p.f = L.f;
   const size_t stage_bytes = size_t(L.R) * kTile * sizeof(float);
-  int stages = static_cast<int>((96 * 1024) / stage_bytes);
+  int stages = static_cast<int>((200 * 1024) / stage_bytes);
   stages = max(2, min(8, stages));
   p.stages = stages;
   p.num_tiles = (L.d + kTile - 1) / kTile;
   const size_t smem = stages * stage_bytes + 2 * stages * sizeof(uint64_t);
-  auto kern = coord_select_kernel<MODE, N>;
+  auto kern = coord_select_kernel<MODE, N, W>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   int occ = 0;
@@ -252,6 +286,15 @@ inline cudaError_t launch_mode(const CoordLaunch& L, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+template <int MODE, int N>
+inline cudaError_t launch_mode(const CoordLaunch& L, cudaStream_t stream) {
+  if constexpr (N > 0) {
+    return launch_mode_w<MODE, N, consumer_warps<N>()>(L, stream);
+  } else {
+    if (L.R <= 32) return launch_mode_w<MODE, 0, 15>(L, stream);
+    return launch_mode_w<MODE, 0, 7>(L, stream);
+  }
+}
 
 template <int MODE, int LO, int HI>
 inline cudaError_t dispatch_range(const CoordLaunch& L, cudaStream_t stream) {

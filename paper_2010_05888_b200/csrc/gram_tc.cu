@@ -49,13 +49,13 @@ struct Cfg {
   static constexpr int ATOM_BYTES = M * 128;     // one K atom of A (8-row groups of 1 KB)
   static constexpr int OP_BYTES = ATOMS * ATOM_BYTES;      // one operand stage (A; B aliases its H rows)
   static constexpr int OP_STAGES = 2;
-  // Raw ring: one TMA bulk copy per row covers RAW_SUB tiles (2 KB / 768 B per
+  // Raw ring: one TMA bulk copy per row covers RAW_SUB tiles (1.5 KB / 768 B per
   // row): the bulk-copy path is bound by requests, not bytes (tools/membench.cu).
-  static constexpr int RAW_SUB = (NP == 32) ? 4 : 2;
+  static constexpr int RAW_SUB = (NP == 32) ? 3 : 2;
   static constexpr int RAW_KT = RAW_SUB * KT;    // coordinates per raw stage
   static constexpr int RAW_PITCH = RAW_KT * 4 + 16;   // bytes per raw row (+16: conflict-free LDS.128)
   static constexpr int RAW_BYTES = NP * RAW_PITCH;    // one raw stage (TMA destination)
-  static constexpr int RAW_STAGES = 2;
+  static constexpr int RAW_STAGES = (NP == 32) ? 3 : 2;   // ~96 KB / ~50 KB in flight while one drains
   // warp roles: converters | producer | epilogue | MMA.  The CTA's warp count is
   // rounded up to a multiple of 4 for register allocation: 14 / 16 warps -> 128 regs.
   static constexpr int PRODUCER_WARP = CONV_WARPS;
@@ -194,20 +194,27 @@ __device__ int center_pick(const RowPtrs& rows, int n, int64_t d, int64_t k_begi
   }
   named_bar(3, NT);
   // score_i: sum (in j order) of the D_ij whose rank within row i (ties by j)
-  // is below h -- the h smallest
+  // is below h -- the h smallest.  Ranks in parallel over (i, j) pairs.
   const int h = (n - 1) / 2;
-  if (t < n) {
-    float sc = 0.f;
-    for (int j = 0; j < n; ++j) {
-      if (j == t) continue;
-      const float v = Ds[t * (GAR_MAX_N + 1) + j];
+  float* kept = xs;                                        // [64][64] (sample no longer needed)
+  for (int e = t; e < n * n; e += NT) {
+    const int i = e / n, j = e % n;
+    float keep = 0.f;
+    if (i != j) {
+      const float v = Ds[i * (GAR_MAX_N + 1) + j];
       int rk = 0;
       for (int k = 0; k < n; ++k) {
-        const float w = Ds[t * (GAR_MAX_N + 1) + k];
-        rk += (k != t && (w < v || (w == v && k < j))) ? 1 : 0;
+        const float w = Ds[i * (GAR_MAX_N + 1) + k];
+        rk += (k != i && (w < v || (w == v && k < j))) ? 1 : 0;
       }
-      if (rk < h) sc += v;
+      keep = (rk < h) ? v : 0.f;
     }
+    kept[i * GAR_MAX_N + j] = keep;
+  }
+  named_bar(3, NT);
+  if (t < n) {
+    float sc = 0.f;
+    for (int j = 0; j < n; ++j) sc += kept[t * GAR_MAX_N + j];
     score[t] = sc;
   }
   named_bar(3, NT);
@@ -326,7 +333,6 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
       off_hi[u] = (qb >> 3) * C::ATOM_BYTES + sw128_offset(b * NP + r, qb & 7);
       off_lo[u] = (qb >> 3) * C::ATOM_BYTES + sw128_offset(C::N + b * NP + r, qb & 7);
     }
-    static_assert(C::RAW_SUB % C::OP_STAGES == 0, "operand stage = sub % OP_STAGES");
     const int64_t R = (T + C::RAW_SUB - 1) / C::RAW_SUB;
     for (int64_t j = 0; j < R; ++j) {
       const int rs = static_cast<int>(j % C::RAW_STAGES);
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
       for (int sub = 0; sub < C::RAW_SUB; ++sub) {
         const int64_t i = j * C::RAW_SUB + sub;
         if (i >= T) break;
-        const int s = sub % C::OP_STAGES;
+        const int s = static_cast<int>(i % C::OP_STAGES);
         const unsigned char* rt = raw_me + rs * C::RAW_BYTES + sub * C::KT * 4;
         const unsigned char* rtc = raw_c + rs * C::RAW_BYTES + sub * C::KT * 4;
         // the tile holding coordinate d-1 may end in a (< 4-coordinate) chunk the
