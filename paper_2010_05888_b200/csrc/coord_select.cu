@@ -5,6 +5,32 @@
 
 namespace gar {
 
+// Krum combine (one selected row): out = fp32((0 + x) / 1) = x + 0 (-0 -> +0),
+// a plain vectorised streaming copy.
+__global__ void __launch_bounds__(256) copy_row_kernel(const __grid_constant__ RowPtrs rows, const int32_t* idx,
+                                                        float* __restrict__ out, int64_t d) {
+  const float* src = rows.p[idx ? idx[0] : 0];
+  const int64_t n4 = d >> 2;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n4; q += int64_t(gridDim.x) * blockDim.x) {
+    float4 v = __ldcs(reinterpret_cast<const float4*>(src) + q);
+    v.x = __fadd_rn(v.x, 0.0f); v.y = __fadd_rn(v.y, 0.0f); v.z = __fadd_rn(v.z, 0.0f); v.w = __fadd_rn(v.w, 0.0f);
+    __stcs(reinterpret_cast<float4*>(out) + q, v);
+  }
+  const int64_t k = (n4 << 2) + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (blockIdx.x == 0 && k < d) out[k] = __fadd_rn(src[k], 0.0f);
+}
+
+inline cudaError_t launch_copy_row(const CoordLaunch& L, cudaStream_t stream) {
+  RowPtrs rp;
+  for (int i = 0; i < GAR_MAX_N; ++i) rp.p[i] = (i < L.n) ? L.rows[i] : nullptr;
+  int64_t blocks = (L.d / 4 + 255) / 256;
+  const int64_t cap = int64_t(L.num_sms) * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  copy_row_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(rp, L.idx, L.out, L.d);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_coord_median_1_16(const CoordLaunch& L, cudaStream_t stream);
 cudaError_t launch_coord_median_17_32(const CoordLaunch& L, cudaStream_t stream);
 cudaError_t launch_coord_median_33_48(const CoordLaunch& L, cudaStream_t stream);
