@@ -161,49 +161,34 @@ def run_ours(args):
     X = synth.make_gradients(n, f, dl, seed=synth.BASE_SEED + 2 + 1000 * rank, device=dev)
     torch.cuda.synchronize()
 
-    aggs = {r: gar.init(r, n, f) for r in RULES}
+    from paper_2010_05888_b200.dist import ShardedAggregator, shard_len
+    aggs = {r: ShardedAggregator(r, n, f, d, output=args.output) for r in RULES}
     outs = {r: torch.empty(dl, dtype=torch.float32, device=dev) for r in RULES}
-    per = synth.shard_bounds(d, 0, world)[1] if world > 1 else d
-    full = {r: torch.empty(per * world, dtype=torch.float32, device=dev) for r in RULES} if world > 1 else None
-    padded = torch.zeros(per, dtype=torch.float32, device=dev) if world > 1 else None
-    ws = torch.empty(max(gar.gar_workspace_bytes(r, n, f, dl) for r in KRUM), dtype=torch.uint8, device=dev)
-    G = torch.empty((n, n), dtype=torch.float64, device=dev)
-    idx = {r: torch.empty(64, dtype=torch.int32, device=dev) for r in KRUM}
+    full = {r: torch.empty(shard_len(d, world) * world, dtype=torch.float32, device=dev) for r in RULES} \
+        if world > 1 else {r: None for r in RULES}
     stream = torch.cuda.current_stream(dev)
-
+    # kernel class of the stage ending at each mark (DESIGN.md §8 roofline bookkeeping)
+    CLASS = {"gram": "gram", "exchange": "exchange", "select": "select", "combine": "coord_select",
+             "coord": "coord_select", "gather": "gather"}
     segs = []          # (kernel class, rule, start event, end event)
 
-    def mark():
+    def ev():
         e = torch.cuda.Event(enable_timing=True)
         e.record(stream)
         return e
 
     def step(record):
-        for r in ("average", "median", "trimmed_mean"):
-            a = mark() if record else None
-            aggs[r].aggregate(X, out=outs[r], d=dl)
-            if record:
-                segs.append(("coord_select", r, a, mark()))
-            if world > 1 and args.output == "replicated":
-                padded[:dl].copy_(outs[r])
-                dist.all_gather_into_tensor(full[r], padded)
-        for r in KRUM:
-            a = mark() if record else None
-            gar.gar_gram_partial(X, G, ws, d=dl)
-            b = mark() if record else None
-            if world > 1:
-                dist.all_reduce(G)
-            c = mark() if record else None
-            gar.gar_select_from_gram(r, G, n, f, 0, idx[r])
-            e1 = mark() if record else None
-            gar.gar_combine(r, X, f, 0, idx[r], outs[r], d=dl)
-            if record:
-                e2 = mark()
-                segs.extend([("gram", r, a, b), ("exchange", r, b, c), ("select", r, c, e1),
-                             ("coord_select", r, e1, e2)])
-            if world > 1 and args.output == "replicated":
-                padded[:dl].copy_(outs[r])
-                dist.all_gather_into_tensor(full[r], padded)
+        for r in RULES:
+            if not record:
+                aggs[r].aggregate(X, out_local=outs[r], out_full=full[r])
+                continue
+            last = [ev()]
+
+            def mark(label, r=r, last=last):
+                e = ev()
+                segs.append((CLASS[label], r, last[0], e))
+                last[0] = e
+            aggs[r].aggregate(X, out_local=outs[r], out_full=full[r], mark=mark)
 
     for _ in range(args.warmup):
         step(False)
@@ -212,10 +197,10 @@ def run_ours(args):
         dist.barrier()
     with Clocks(local) as clk:
         torch.cuda.synchronize()
-        t0 = mark()
+        t0 = ev()
         for _ in range(args.steps):
             step(True)
-        t1 = mark()
+        t1 = ev()
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -241,13 +226,13 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        a = mark()
+        a = ev()
         for _ in range(args.e2e_steps):
             X.copy_(host_x, non_blocking=True)
             for r in RULES:
-                aggs[r].aggregate(X, out=outs[r], d=dl)
-                host_out[r].copy_(outs[r], non_blocking=True)
-        b = mark()
+                res = aggs[r].aggregate(X, out_local=outs[r], out_full=full[r])
+                host_out[r].copy_(res[:dl] if world == 1 else outs[r], non_blocking=True)
+        b = ev()
         torch.cuda.synchronize()
         e2e_ms = a.elapsed_time(b) / args.e2e_steps
         if world > 1:
@@ -304,7 +289,7 @@ def run_ours(args):
         "gpu_launches": 15 * args.steps, "e2e": e2e,
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, sample_d=1 << 20)
+        line["cpu_baseline"] = cpu_baseline(cfg, X, d)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -317,16 +302,23 @@ def oracle_step(x, f):
         oracle.aggregate(r, x, f)
 
 
-def cpu_baseline(cfg, sample_d):
+def cpu_baseline(cfg, X, d, reps=3):
+    """The oracle, as it stands, on the box's host cores over the SAME resident
+    workload (copied to host): all six GARs once per repetition, median of
+    `reps` (about 10-30 s of CPU work at C3)."""
     import oracle
-    x = synth.make_gradients(cfg.n, cfg.f, sample_d, seed=synth.BASE_SEED + 2, ld=sample_d).numpy()
-    t = time.perf_counter()
-    oracle_step(x, cfg.f)
-    dt = time.perf_counter() - t
-    return {"value": round(len(RULES) * cfg.n * sample_d * 4 / dt / 1e9, 4), "unit": "GB/s",
+    x = X[:, :d].cpu().numpy()
+    x = x if x.flags["C_CONTIGUOUS"] else x.copy()
+    times = []
+    for _ in range(reps):
+        t = time.perf_counter()
+        oracle_step(x, cfg.f)
+        times.append(time.perf_counter() - t)
+    dt = statistics.median(times)
+    return {"value": round(len(RULES) * cfg.n * d * 4 / dt / 1e9, 4), "unit": "GB/s",
             "cores": oracle.default_threads(), "kind": "oracle",
-            "sample": f"first-draw {cfg.name} shape, n={cfg.n} f={cfg.f}, d={sample_d} coordinates, all six GARs "
-                      f"once ({dt:.2f} s)"}
+            "sample": f"the full {cfg.name} workload (n={cfg.n} f={cfg.f} d={d}, same bits as the GPU run), "
+                      f"all six GARs, median of {reps} passes ({dt:.2f} s per pass)"}
 
 
 def run_reference(args):
@@ -335,7 +327,7 @@ def run_reference(args):
         return
     import oracle
     cfg = workload(args.workload)
-    sample_d = 1 << 18
+    sample_d = 1 << 21
     x = synth.make_gradients(cfg.n, cfg.f, sample_d, seed=synth.BASE_SEED + 2, ld=sample_d).numpy()
     for _ in range(args.warmup):
         oracle_step(x, cfg.f)

@@ -43,10 +43,21 @@ struct CoordParams {
 };
 
 // ---------------------------------------------------------------- per-mode math
-// Average over R values in index order, fp64 (R2).
+// Average over R values in index order, fp64 (R2).  The additions stay in
+// index order (bit-exact against the oracle even when the fp64 sum rounds);
+// loads and conversions are batched 8 at a time ahead of the dependent DADD
+// chain so it is not serialised behind LDS/F2F latency.
 __device__ __forceinline__ float avg_column(const float* col, int R, int stride) {
   double s = 0.0;
-  for (int i = 0; i < R; ++i) s += static_cast<double>(col[i * stride]);
+  int i = 0;
+  for (; i + 8 <= R; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = static_cast<double>(col[(i + u) * stride]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; i < R; ++i) s += static_cast<double>(col[i * stride]);
   return static_cast<float>(s / R);
 }
 

@@ -1,0 +1,153 @@
+"""d-sharded multi-GPU aggregation (north_star "Partitioning
+across the 8xB200 box by sharding d").
+
+Rank r of G holds coordinates [lo_r, hi_r) of every one of the n gradients
+(``shard_bounds``: contiguous slices, boundaries at multiples of 1024
+coordinates).  Then:
+
+* Average / Median / trimmed mean and the Bulyan coordinate phase are purely
+  per-coordinate: each rank aggregates its own slice, no communication;
+* Krum / Multi-Krum / Bulyan need the n x n distance matrix of the WHOLE
+  vectors: each rank computes the partial Gram matrix of its slice
+  (``gar_gram_partial``), one all-reduce (SUM, fp64, n*n*8 <= 32 KB) over NCCL
+  sums them (the centring of the Gram is per coordinate, so partial Grams of
+  disjoint slices add up exactly), every rank runs the identical deterministic
+  selection (``gar_select_from_gram``) and combines its own slice
+  (``gar_combine``);
+* the aggregate is all-gathered (``output="replicated"``, the north_star
+  default) or left d-sharded (``output="sharded"``, what a ZeRO-style
+  optimizer consumes).
+
+The paper's own exchange is PyTorch ``broadcast``/``gather`` over NCCL or gloo
+(§4.2); here the only collectives are one tiny
+all-reduce per Krum-family call and the optional output all-gather.
+
+The kernels are reached through ``backend`` (default: libgar).  Tests inject a
+host-side stand-in to exercise the sharding and exchange logic over gloo on CPU.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+KRUM_FAMILY = ("krum", "multi_krum", "bulyan")
+
+
+def shard_bounds(d: int, rank: int, world: int, align: int = 1024) -> tuple[int, int]:
+    """Contiguous slice [lo, hi) of rank `rank`; every slice but the last has
+    the same length, a multiple of `align` coordinates (16-byte row alignment)."""
+    per = (d + world - 1) // world
+    per = (per + align - 1) // align * align
+    lo = min(d, rank * per)
+    hi = min(d, lo + per)
+    return lo, hi
+
+
+def shard_len(d: int, world: int, align: int = 1024) -> int:
+    return shard_bounds(d, 0, world, align)[1] if world > 1 else d
+
+
+class _LibgarBackend:
+    """The product kernels (libgar C ABI)."""
+
+    def __init__(self):
+        from . import _lib
+        self._lib = _lib
+
+    def coordinatewise(self, agg, rows, out, d):
+        agg.aggregate(rows, out=out, d=d)
+
+    def gram_partial(self, rows, gram, ws, d):
+        self._lib.gar_gram_partial(rows, gram, ws, d=d)
+
+    def select_from_gram(self, rule, gram, n, f, m, idx):
+        return self._lib.gar_select_from_gram(rule, gram, n, f, m, idx)
+
+    def combine(self, rule, rows, f, m, idx, out, d):
+        self._lib.gar_combine(rule, rows, f, m, idx, out, d=d)
+
+
+class ShardedAggregator:
+    """``init(name, n, f)`` / ``aggregate`` over a d-sharded
+    process group: one process per GPU, each holding its slice of every row."""
+
+    def __init__(self, rule: str, n: int, f: int, d: int, m: int | None = None, group=None,
+                 output: str = "replicated", backend=None):
+        if output not in ("replicated", "sharded"):
+            raise ValueError(output)
+        self.rule, self.n, self.f, self.d = rule, int(n), int(f), int(d)
+        self.m = 0 if m is None else int(m)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.lo, self.hi = shard_bounds(self.d, self.rank, self.world) if self.world > 1 else (0, self.d)
+        self.d_local = self.hi - self.lo
+        self.per = shard_len(self.d, self.world)
+        self.output = output
+        self.backend = backend if backend is not None else _LibgarBackend()
+        self._agg = None
+        self._ws = None
+        self._gram = None
+        self._idx = None
+        self._pad = None
+
+    # -- lazily created per-device state ------------------------------------------
+    def _state(self, device):
+        if self.rule in KRUM_FAMILY:
+            if self._gram is None:
+                from . import _lib
+                nbytes = max(_lib.gar_workspace_bytes(self.rule, self.n, self.f, self.d_local), 1) \
+                    if device.type == "cuda" else 1
+                self._ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+                self._gram = torch.empty((self.n, self.n), dtype=torch.float64, device=device)
+                self._idx = torch.empty(64, dtype=torch.int32, device=device)
+        elif self._agg is None and device.type == "cuda":
+            from .gar import init
+            self._agg = init(self.rule, self.n, self.f, self.m or None)
+
+    def aggregate(self, rows_local, out_local: torch.Tensor | None = None,
+                  out_full: torch.Tensor | None = None, mark=None) -> torch.Tensor:
+        """rows_local: [n, >= d_local] slice of the gradients.  Returns the
+        local slice (output="sharded") or the whole aggregate (replicated).
+        `mark(label)`, if given, is called after each stage ("gram",
+        "exchange", "select", "combine", "coord", "gather") — the benchmark
+        records CUDA events there."""
+        dev = rows_local.device if isinstance(rows_local, torch.Tensor) else rows_local[0].device
+        self._state(dev)
+        mark = mark or (lambda label: None)
+        if out_local is None:
+            out_local = torch.empty(self.d_local, dtype=torch.float32, device=dev)
+        if self.rule in KRUM_FAMILY:
+            self.backend.gram_partial(rows_local, self._gram, self._ws, self.d_local)
+            mark("gram")
+            if self.world > 1:
+                dist.all_reduce(self._gram, op=dist.ReduceOp.SUM, group=self.group)
+            mark("exchange")
+            self.backend.select_from_gram(self.rule, self._gram, self.n, self.f, self.m, self._idx)
+            mark("select")
+            self.backend.combine(self.rule, rows_local, self.f, self.m, self._idx, out_local, self.d_local)
+            mark("combine")
+        else:
+            self.backend.coordinatewise(self._agg, rows_local, out_local, self.d_local)
+            mark("coord")
+        if self.output == "sharded" or self.world == 1:
+            return out_local
+        if out_full is None:
+            out_full = torch.empty(self.per * self.world, dtype=torch.float32, device=dev)
+        if self.d_local == self.per:
+            dist.all_gather_into_tensor(out_full, out_local, group=self.group)
+        else:
+            if self._pad is None:
+                self._pad = torch.zeros(self.per, dtype=torch.float32, device=dev)
+            self._pad[: self.d_local].copy_(out_local)
+            dist.all_gather_into_tensor(out_full, self._pad, group=self.group)
+        mark("gather")
+        return out_full[: self.d]
+
+    @property
+    def selected(self) -> torch.Tensor | None:
+        """Indices chosen by the last Krum-family call (device int32)."""
+        if self._idx is None:
+            return None
+        from . import _lib
+        return self._idx[: _lib.gar_num_selected(self.rule, self.n, self.f, self.m)]
