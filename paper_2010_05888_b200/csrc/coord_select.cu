@@ -1,6 +1,8 @@
 // coord_select.cu — host dispatch of the coordinate-selection kernel by
 // (mode, rows).  Kernel body: coord_select_impl.cuh; instantiations are split
 // over coord_inst_*.cu so they compile in parallel.
+#include <cstdlib>
+
 #include "coord_select_impl.cuh"
 
 namespace gar {
@@ -18,6 +20,26 @@ __global__ void __launch_bounds__(256) copy_row_kernel(const __grid_constant__ R
   }
   const int64_t k = (n4 << 2) + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (blockIdx.x == 0 && k < d) out[k] = __fadd_rn(src[k], 0.0f);
+}
+
+int l2_evict_first_enabled() {
+  static const int v = [] {
+    const char* e = getenv("GAR_L2_EVICT_FIRST");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  return v;
+}
+
+int coord_loader_ldg(int mode, int R) {
+  static const int forced = [] {
+    const char* e = getenv("GAR_COORD_LOADER");
+    if (e && e[0] == 'l') return 1;
+    if (e && e[0] == 't') return 0;
+    return -1;
+  }();
+  if (forced >= 0) return forced;
+  if ((mode == kModeMedian || mode == kModeTrimmed) && R <= 32) return 0;
+  return 1;
 }
 
 inline cudaError_t launch_copy_row(const CoordLaunch& L, cudaStream_t stream) {

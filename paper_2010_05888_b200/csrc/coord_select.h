@@ -20,4 +20,8 @@ struct CoordLaunch {
 
 cudaError_t launch_coord_select(int mode, const CoordLaunch& L, cudaStream_t stream);
 
+// Tuning knob: L2 evict-first policy on the streaming bulk copies (default off:
+// measured no gain; GAR_L2_EVICT_FIRST=1 enables it).  Read once per process.
+int l2_evict_first_enabled();
+
 }  // namespace gar

@@ -39,6 +39,7 @@ struct CoordParams {
   int R;                // rows consumed per coordinate
   int f;                // trimmed mean: trim per side; Bulyan: declared f
   int stages;
+  int l2_hint;          // 1: bulk copies carry an L2 evict-first policy
   int64_t num_tiles;
 };
 
@@ -194,7 +195,11 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) coord_select_kernel(const __g
         mbar_arrive_expect_tx(&full[stage], bytes * R);
         if (bytes) {
           float* dst = tiles + size_t(stage) * R * kTile;
-          for (int r = 0; r < R; ++r) bulk_g2s(dst + r * kTile, rowp[r] + start, bytes, &full[stage], pol);
+          if (p.l2_hint) {
+            for (int r = 0; r < R; ++r) bulk_g2s(dst + r * kTile, rowp[r] + start, bytes, &full[stage], pol);
+          } else {
+            for (int r = 0; r < R; ++r) bulk_g2s_plain(dst + r * kTile, rowp[r] + start, bytes, &full[stage]);
+          }
         }
         if (++stage == stages) { stage = 0; phase ^= 1; }
       }
@@ -240,6 +245,103 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) coord_select_kernel(const __g
   }
 }
 
+// ---------------------------------------------------------------- LDG variant
+// Direct-load variant: thread = coordinate, its R values are loaded straight into
+// registers (coalesced 128 B per warp and row, streaming), no staging.  The
+// register file (256 KB/SM) holds more in-flight data than the shared-memory
+// ring, which matters for large R (tools/membench.cu: ~6.5 TB/s at any R with
+// >= 32 warps/SM).  Bulyan's runtime-offset window reads use a per-thread
+// shared-memory column.
+constexpr int kLdgThreads = 256;
+
+template <int MODE, int N>
+__global__ void __launch_bounds__(kLdgThreads) coord_ldg_kernel(const __grid_constant__ CoordParams p) {
+  extern __shared__ __align__(16) unsigned char ldg_smem[];
+  __shared__ const float* rowp[GAR_MAX_N];
+  __shared__ int sel_s[GAR_MAX_N];
+  const int R = (N > 0) ? N : p.R;
+  if (threadIdx.x == 0) {
+    if (p.idx) {
+      for (int r = 0; r < R; ++r) {
+        int v = p.idx[r], t = r;
+        while (t > 0 && sel_s[t - 1] > v) { sel_s[t] = sel_s[t - 1]; --t; }
+        sel_s[t] = v;
+      }
+      for (int r = 0; r < R; ++r) rowp[r] = p.rows.p[sel_s[r]];
+    } else {
+      for (int r = 0; r < R; ++r) rowp[r] = p.rows.p[r];
+    }
+  }
+  __syncthreads();
+  const int64_t d = p.d;
+  const int64_t step = int64_t(gridDim.x) * kLdgThreads;
+  for (int64_t k = int64_t(blockIdx.x) * kLdgThreads + threadIdx.x; k < d; k += step) {
+    float res;
+    if constexpr (MODE == kModeAverage) {
+      double s = 0.0;
+      int i = 0;
+      for (; i + 16 <= R; i += 16) {
+        float v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = __ldcs(rowp[i + u] + k);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) s += static_cast<double>(v[u]);
+      }
+      for (; i < R; ++i) s += static_cast<double>(__ldcs(rowp[i] + k));
+      res = static_cast<float>(s / R);
+    } else {
+      float v[N];
+#pragma unroll
+      for (int r = 0; r < N; ++r) v[r] = __ldcs(rowp[r] + k);
+#pragma unroll
+      for (int r = 0; r < N; ++r) v[r] = canon(v[r]);
+      if constexpr (MODE == kModeMedian) {
+        res = median_column<N>(v);
+      } else if constexpr (MODE == kModeTrimmed) {
+        res = trimmed_column<N>(v, p.f);
+      } else {
+        float* col = reinterpret_cast<float*>(ldg_smem) + threadIdx.x;
+        res = bulyan_column<N>(v, col, kLdgThreads, p.f, rowp, k);
+      }
+    }
+    __stcs(p.out + k, res);
+  }
+}
+
+template <int MODE, int N>
+inline cudaError_t launch_ldg(const CoordLaunch& L, cudaStream_t stream) {
+  CoordParams p;
+  for (int i = 0; i < GAR_MAX_N; ++i) p.rows.p[i] = (i < L.n) ? L.rows[i] : nullptr;
+  p.idx = L.idx;
+  p.out = L.out;
+  p.d = L.d;
+  p.R = L.R;
+  p.f = L.f;
+  p.stages = 0;
+  p.l2_hint = 0;
+  p.num_tiles = 0;
+  const size_t smem = (MODE == kModeBulyan) ? size_t(L.R) * kLdgThreads * sizeof(float) : 0;
+  auto kern = coord_ldg_kernel<MODE, N>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kLdgThreads, smem);
+  if (e != cudaSuccess) return e;
+  occ = max(1, occ);
+  int64_t grid = int64_t(L.num_sms) * occ;
+  const int64_t need = (L.d + kLdgThreads - 1) / kLdgThreads;
+  if (grid > need) grid = need > 0 ? need : 1;
+  kern<<<static_cast<unsigned>(grid), kLdgThreads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+// Loader selection (measured on B200, tools/ab_step.py): the TMA ring wins for
+// the network-heavy Median / trimmed mean up to 32 rows (loads overlap the
+// ALU-bound networks); direct loads win for Average at every R, for the Bulyan
+// phase, and for anything above 32 rows.  GAR_COORD_LOADER=tma|ldg forces one.
+// Returns 1 for LDG.
+int coord_loader_ldg(int mode, int R);
+
 // ---------------------------------------------------------------- host side
 template <int MODE, int N, int W>
 inline cudaError_t launch_mode_w(const CoordLaunch& L, cudaStream_t stream) {
@@ -256,6 +358,7 @@ inline cudaError_t launch_mode_w(const CoordLaunch& L, cudaStream_t stream) {
   int stages = static_cast<int>((200 * 1024) / stage_bytes);
   stages = max(2, min(8, stages));
   p.stages = stages;
+  p.l2_hint = l2_evict_first_enabled();
   p.num_tiles = (L.d + kTile - 1) / kTile;
   const size_t smem = stages * stage_bytes + 2 * stages * sizeof(uint64_t);
   auto kern = coord_select_kernel<MODE, N, W>;
@@ -273,6 +376,7 @@ inline cudaError_t launch_mode_w(const CoordLaunch& L, cudaStream_t stream) {
 
 template <int MODE, int N>
 inline cudaError_t launch_mode(const CoordLaunch& L, cudaStream_t stream) {
+  if (coord_loader_ldg(MODE, L.R)) return launch_ldg<MODE, N>(L, stream);
   if constexpr (N > 0) {
     return launch_mode_w<MODE, N, consumer_warps<N>()>(L, stream);
   } else {

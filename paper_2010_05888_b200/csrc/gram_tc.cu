@@ -24,6 +24,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "coord_select.h"
 #include "gram.h"
 
 namespace gar {
@@ -228,7 +229,7 @@ __device__ int center_pick(const RowPtrs& rows, int n, int64_t d, int64_t k_begi
 template <int NP>
 __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
     gram_tc_kernel(const __grid_constant__ RowPtrs rows, int n, int64_t d, int64_t num_tiles,
-                   double* __restrict__ partials) {
+                   double* __restrict__ partials, int l2_hint) {
   using C = Cfg<NP>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment (SWIZZLE_128B) by offsetting the shared array itself, so
@@ -298,7 +299,10 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
 #pragma unroll
         for (int u = 0; u < NP / 32; ++u) {
           const int r = lane + 32 * u;
-          if (r < n) bulk_g2s(dst + r * C::RAW_PITCH, rows.p[r] + k0, bytes, &raw_full[rs], pol);
+          if (r < n) {
+            if (l2_hint) bulk_g2s(dst + r * C::RAW_PITCH, rows.p[r] + k0, bytes, &raw_full[rs], pol);
+            else bulk_g2s_plain(dst + r * C::RAW_PITCH, rows.p[r] + k0, bytes, &raw_full[rs]);
+          }
         }
       }
     }
@@ -480,7 +484,8 @@ cudaError_t launch_np(const RowPtrs& rp, int n, int64_t d, double* partials, int
   cudaError_t e = cudaFuncSetAttribute(gram_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        C::SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  gram_tc_kernel<NP><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(rp, n, d, tiles, partials);
+  gram_tc_kernel<NP><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(rp, n, d, tiles, partials,
+                                                                   l2_evict_first_enabled());
   *n_parts = grid;
   return cudaGetLastError();
 }
