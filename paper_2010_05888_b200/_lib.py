@@ -76,15 +76,40 @@ def rule_id(rule) -> int:
     return int(rule)
 
 
+_PTR_CACHE: dict = {}
+
+
 def row_pointers(grads, d: int | None = None):
     """(ctypes void* array, n, d) from a list of 1-D fp32 CUDA tensors or a
-    2-D [n, ld] fp32 CUDA tensor with unit column stride."""
+    2-D [n, ld] fp32 CUDA tensor with unit column stride.  For a matrix the
+    row pointers are base + i * row_stride (no per-row tensor views), and the
+    ctypes array is cached per (base, n, stride)."""
     if isinstance(grads, torch.Tensor):
         if grads.dim() != 2:
             raise ValueError("a gradient matrix must be 2-D [n, ld]")
-        rows = [grads[i] for i in range(grads.shape[0])]
-    else:
-        rows = list(grads)
+        if grads.dtype != torch.float32:
+            raise TypeError("gradients must be float32")
+        if grads.device.type != "cuda":
+            raise ValueError("gradients must live on a CUDA device (no CPU fallback)")
+        n, ld = grads.shape
+        if not 1 <= n <= MAX_N:
+            raise ValueError(f"n = {n} outside [1, {MAX_N}]")
+        if ld > 1 and grads.stride(1) != 1:
+            raise ValueError("gradient rows must be contiguous")
+        if d is None:
+            d = ld
+        elif d > ld:
+            raise ValueError("a gradient is shorter than d")
+        base, rs = grads.data_ptr(), grads.stride(0) * 4
+        key = (base, n, rs)
+        arr = _PTR_CACHE.get(key)
+        if arr is None:
+            if len(_PTR_CACHE) > 256:
+                _PTR_CACHE.clear()
+            arr = (ctypes.c_void_p * n)(*[base + i * rs for i in range(n)])
+            _PTR_CACHE[key] = arr
+        return arr, n, d, grads.device
+    rows = list(grads)
     n = len(rows)
     if not 1 <= n <= MAX_N:
         raise ValueError(f"n = {n} outside [1, {MAX_N}]")

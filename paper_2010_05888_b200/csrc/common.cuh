@@ -3,6 +3,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #define GAR_MAX_N 64
 
 namespace gar {
@@ -84,5 +86,48 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // Canonical value for order statistics (R1): NaN -> +inf, -0 -> +0.
 // fminf(NaN, +inf) = +inf (min returns the non-NaN operand); x + 0 maps -0 to +0.
 __device__ __forceinline__ float canon(float v) { return __fadd_rn(fminf(v, __int_as_float(0x7f800000)), 0.0f); }
+
+// Host helper: set the dynamic shared-memory limit of `kern` and query its
+// occupancy once per (kernel, device, smem size); both calls cost microseconds,
+// which dominate small aggregations.
+template <class K>
+inline cudaError_t cached_occupancy(K kern, int threads, size_t smem, int* occ) {
+  // keyed by the kernel's address: instantiations of one template share the type K
+  struct Entry {
+    const void* fn = nullptr;
+    int device = -1;
+    int threads = 0;
+    size_t smem = 0;
+    int occ = 0;
+  };
+  static Entry cache[64];
+  static int next = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const void* fn = reinterpret_cast<const void*>(kern);
+  for (const Entry& c : cache)
+    if (c.fn == fn && c.device == dev && c.threads == threads && c.smem == smem) {
+      *occ = c.occ;
+      return cudaSuccess;
+    }
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int o = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem);
+  if (e != cudaSuccess) return e;
+  o = o > 0 ? o : 1;
+  Entry& c = cache[next];
+  next = (next + 1) % 64;
+  c.fn = fn;
+  c.device = dev;
+  c.threads = threads;
+  c.smem = smem;
+  c.occ = o;
+  *occ = o;
+  return cudaSuccess;
+}
 
 }  // namespace gar

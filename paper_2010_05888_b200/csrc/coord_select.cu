@@ -38,7 +38,7 @@ int coord_loader_ldg(int mode, int R) {
     return -1;
   }();
   if (forced >= 0) return forced;
-  if ((mode == kModeMedian || mode == kModeTrimmed) && R <= 32) return 0;
+  if (mode != kModeBulyan && R <= 32) return 0;
   return 1;
 }
 

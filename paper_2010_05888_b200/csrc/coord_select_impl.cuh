@@ -23,11 +23,14 @@
 
 namespace gar {
 
-// W consumer warps (one coordinate per thread per tile) + 1 producer warp.
-// W = 15 for up to 32 rows: 480-coordinate tiles = 1920 B per row per bulk
-// copy, 16 warps per CTA (128 registers), one CTA per SM with a ~180 KB ring;
-// W = 7 above 32 rows keeps 3 stages of 63 rows in shared memory.  Large
-// copies matter: the bulk-copy path is bound by requests (tools/membench.cu).
+// W consumer warps (one coordinate per thread per tile) + kProducers producer
+// warps.  W = 15 for up to 32 rows: 480-coordinate tiles = 1920 B per row per
+// bulk copy, one CTA per SM with a ~180 KB ring; W = 7 above 32 rows keeps 3
+// stages of 63 rows in shared memory.  Copy size AND the number of issuing
+// warps matter: bulk-copy issue is limited per warp (tools/membench2.cu:
+// 31 rows x 1 KB go 1.3 -> 5.5 TB/s from 1 to 8 issuing warps), so producer
+// warp p issues rows r = p mod kProducers and arms its own stage barrier.
+constexpr int kProducers = 4;
 template <int N>
 constexpr int consumer_warps() { return N <= 32 ? 15 : 7; }
 
@@ -147,15 +150,15 @@ __device__ __forceinline__ float bulyan_column(float* v, float* col, int stride,
 
 // ---------------------------------------------------------------- the kernel
 template <int MODE, int N, int W>
-__global__ void __launch_bounds__(32 * (W + 1), 1) coord_select_kernel(const __grid_constant__ CoordParams p) {
+__global__ void __launch_bounds__(32 * (W + kProducers), 1) coord_select_kernel(const __grid_constant__ CoordParams p) {
   constexpr int kConsumerWarps = W;
   constexpr int kTile = 32 * W;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int R = (N > 0) ? N : p.R;
   const int stages = p.stages;
   float* tiles = reinterpret_cast<float*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + size_t(stages) * R * kTile * sizeof(float));
-  uint64_t* empty = full + stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + size_t(stages) * R * kTile * sizeof(float));  // [stages][kProducers]
+  uint64_t* empty = full + stages * kProducers;
   __shared__ const float* rowp[GAR_MAX_N];
   __shared__ int sel_s[GAR_MAX_N];
 
@@ -173,7 +176,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) coord_select_kernel(const __g
       for (int r = 0; r < R; ++r) rowp[r] = p.rows.p[r];
     }
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
+      for (int q = 0; q < kProducers; ++q) mbar_init(&full[s * kProducers + q], 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
     fence_mbar_init();
@@ -181,10 +184,12 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) coord_select_kernel(const __g
   __syncthreads();
 
   const int64_t d = p.d;
-  if (warp == kConsumerWarps) {
-    // ------------------------------------------------ producer (TMA bulk)
+  if (warp >= kConsumerWarps) {
+    // ------------------------------------------------ producers (TMA bulk)
+    const int q = warp - kConsumerWarps;           // rows r = q (mod kProducers)
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
+      const int my_rows = (R > q) ? (R - q + kProducers - 1) / kProducers : 0;
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
@@ -192,13 +197,14 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) coord_select_kernel(const __g
         const int64_t start = tile * kTile;
         const int cnt = static_cast<int>((d - start < kTile ? d - start : int64_t(kTile)));
         const uint32_t bytes = static_cast<uint32_t>(cnt & ~3) * 4u;
-        mbar_arrive_expect_tx(&full[stage], bytes * R);
+        uint64_t* bar = &full[stage * kProducers + q];
+        mbar_arrive_expect_tx(bar, bytes * my_rows);
         if (bytes) {
           float* dst = tiles + size_t(stage) * R * kTile;
           if (p.l2_hint) {
-            for (int r = 0; r < R; ++r) bulk_g2s(dst + r * kTile, rowp[r] + start, bytes, &full[stage], pol);
+            for (int r = q; r < R; r += kProducers) bulk_g2s(dst + r * kTile, rowp[r] + start, bytes, bar, pol);
           } else {
-            for (int r = 0; r < R; ++r) bulk_g2s_plain(dst + r * kTile, rowp[r] + start, bytes, &full[stage]);
+            for (int r = q; r < R; r += kProducers) bulk_g2s_plain(dst + r * kTile, rowp[r] + start, bytes, bar);
           }
         }
         if (++stage == stages) { stage = 0; phase ^= 1; }
@@ -212,7 +218,8 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) coord_select_kernel(const __g
   uint32_t phase = 0;
   const int c = threadIdx.x;
   for (int64_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-    mbar_wait(&full[stage], phase);
+#pragma unroll
+    for (int q = 0; q < kProducers; ++q) mbar_wait(&full[stage * kProducers + q], phase);
     const int64_t start = tile * kTile;
     const int cnt = static_cast<int>((d - start < kTile ? d - start : int64_t(kTile)));
     const int bulk_cnt = cnt & ~3;
@@ -322,12 +329,9 @@ inline cudaError_t launch_ldg(const CoordLaunch& L, cudaStream_t stream) {
   p.num_tiles = 0;
   const size_t smem = (MODE == kModeBulyan) ? size_t(L.R) * kLdgThreads * sizeof(float) : 0;
   auto kern = coord_ldg_kernel<MODE, N>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kLdgThreads, smem);
+  cudaError_t e = cached_occupancy(kern, kLdgThreads, smem, &occ);
   if (e != cudaSuccess) return e;
-  occ = max(1, occ);
   int64_t grid = int64_t(L.num_sms) * occ;
   const int64_t need = (L.d + kLdgThreads - 1) / kLdgThreads;
   if (grid > need) grid = need > 0 ? need : 1;
@@ -335,10 +339,11 @@ inline cudaError_t launch_ldg(const CoordLaunch& L, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-// Loader selection (measured on B200, tools/ab_step.py): the TMA ring wins for
-// the network-heavy Median / trimmed mean up to 32 rows (loads overlap the
-// ALU-bound networks); direct loads win for Average at every R, for the Bulyan
-// phase, and for anything above 32 rows.  GAR_COORD_LOADER=tma|ldg forces one.
+// Loader selection (measured on B200, tools/ab_step.py): with 4 issuing warps the
+// TMA ring wins up to 32 rows (C3: Average 0.47 ms vs 0.53, Median 0.52 vs
+// 0.65); direct loads win for the Bulyan phase (its sort-and-window consumer is
+// the bottleneck) and above 32 rows (the ring only fits 896 B copies).
+// GAR_COORD_LOADER=tma|ldg forces one.
 // Returns 1 for LDG.
 int coord_loader_ldg(int mode, int R);
 
@@ -346,7 +351,7 @@ int coord_loader_ldg(int mode, int R);
 template <int MODE, int N, int W>
 inline cudaError_t launch_mode_w(const CoordLaunch& L, cudaStream_t stream) {
   constexpr int kTile = 32 * W;
-  constexpr int kThreads = 32 * (W + 1);
+  constexpr int kThreads = 32 * (W + kProducers);
   CoordParams p;
   for (int i = 0; i < GAR_MAX_N; ++i) p.rows.p[i] = (i < L.n) ? L.rows[i] : nullptr;
   p.idx = L.idx;
@@ -360,14 +365,11 @@ inline cudaError_t launch_mode_w(const CoordLaunch& L, cudaStream_t stream) {
   p.stages = stages;
   p.l2_hint = l2_evict_first_enabled();
   p.num_tiles = (L.d + kTile - 1) / kTile;
-  const size_t smem = stages * stage_bytes + 2 * stages * sizeof(uint64_t);
+  const size_t smem = stages * stage_bytes + (kProducers + 1) * stages * sizeof(uint64_t);
   auto kern = coord_select_kernel<MODE, N, W>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+  cudaError_t e = cached_occupancy(kern, kThreads, smem, &occ);
   if (e != cudaSuccess) return e;
-  occ = max(1, occ);
   int64_t grid = int64_t(L.num_sms) * occ;
   if (grid > p.num_tiles) grid = p.num_tiles > 0 ? p.num_tiles : 1;
   kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(p);

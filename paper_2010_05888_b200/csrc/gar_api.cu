@@ -80,18 +80,54 @@ gar_status check_device_ptr(const void* p) {
   return GAR_OK;
 }
 
+// Pointer-table validation costs one cudaPointerGetAttributes per row; a
+// per-thread cache of recently validated (device, table) pairs lets repeated
+// calls on the same gradient buffers (the normal training-loop case) skip it.
+struct ValidatedSet {
+  int device = -1;
+  int n = 0;
+  const float* p[GAR_MAX_N];
+};
+thread_local ValidatedSet g_validated[4];
+thread_local int g_validated_next = 0;
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  return dev;
+}
+
 gar_status check_device_rows(const float* const* grads, int n, const void* out) {
-  for (int i = 0; i < n; ++i) {
-    gar_status s = check_device_ptr(grads[i]);
-    if (s != GAR_OK) return s;
+  const int dev = current_device();
+  bool cached = false;
+  for (const ValidatedSet& v : g_validated) {
+    if (v.device == dev && v.n == n && std::memcmp(v.p, grads, sizeof(const float*) * n) == 0) {
+      cached = true;
+      break;
+    }
+  }
+  if (!cached) {
+    for (int i = 0; i < n; ++i) {
+      gar_status s = check_device_ptr(grads[i]);
+      if (s != GAR_OK) return s;
+    }
+    ValidatedSet& v = g_validated[g_validated_next];
+    g_validated_next = (g_validated_next + 1) % 4;
+    v.device = dev;
+    v.n = n;
+    std::memcpy(v.p, grads, sizeof(const float*) * n);
   }
   return out ? check_device_ptr(out) : GAR_OK;
 }
 
 int num_sms() {
-  int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  static int cache[64] = {0};
+  const int dev = current_device();
+  if (dev < 0) return 148;
+  if (dev < 64 && cache[dev] > 0) return cache[dev];
+  int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+  if (dev < 64) cache[dev] = sms;
   return sms;
 }
 

@@ -43,24 +43,26 @@ struct Cfg {
   static constexpr int BLOCKS = 64 / NP;         // 2 / 1
   static constexpr int M = 2 * NP * BLOCKS;      // 128: H rows of all blocks, then L rows
   static constexpr int N = NP * BLOCKS;          // 64: H rows of all blocks
-  static constexpr int CONV_WARPS = (NP == 32) ? 8 : 6;   // converters: 16 coordinates each
-  static constexpr int KT = 16 * CONV_WARPS;     // coordinates per tile: 128 / 96
-  static constexpr int KB = KT / BLOCKS;         // coordinates per block (MMA K extent): 64 / 96
+  static constexpr int CONV_WARPS = (NP == 32) ? 8 : 4;   // converters: 16 coordinates each
+  static constexpr int KT = 16 * CONV_WARPS;     // coordinates per tile: 128 / 64
+  static constexpr int KB = KT / BLOCKS;         // coordinates per block (MMA K extent): 64 / 64
   static constexpr int ATOMS = KB / 32;          // 128-byte K atoms per tile
   static constexpr int ATOM_BYTES = M * 128;     // one K atom of A (8-row groups of 1 KB)
   static constexpr int OP_BYTES = ATOMS * ATOM_BYTES;      // one operand stage (A; B aliases its H rows)
   static constexpr int OP_STAGES = 2;
-  // Raw ring: one TMA bulk copy per row covers RAW_SUB tiles (1.5 KB / 768 B per
-  // row): the bulk-copy path is bound by requests, not bytes (tools/membench.cu).
-  static constexpr int RAW_SUB = (NP == 32) ? 3 : 2;
+  // Raw ring: one TMA bulk copy per row covers RAW_SUB tiles (1.5 KB / 1 KB per
+  // row), issued by PROD_WARPS warps (rows r = p mod PROD_WARPS, one barrier
+  // each): bulk-copy issue is limited per request and per issuing warp
+  // (tools/membench.cu, membench2.cu).
+  static constexpr int PROD_WARPS = 3;
+  static constexpr int RAW_SUB = (NP == 32) ? 3 : 4;
   static constexpr int RAW_KT = RAW_SUB * KT;    // coordinates per raw stage
   static constexpr int RAW_PITCH = RAW_KT * 4 + 16;   // bytes per raw row (+16: conflict-free LDS.128)
   static constexpr int RAW_BYTES = NP * RAW_PITCH;    // one raw stage (TMA destination)
   static constexpr int RAW_STAGES = (NP == 32) ? 3 : 2;   // ~96 KB / ~50 KB in flight while one drains
-  // warp roles: converters | producer | epilogue | MMA.  The CTA's warp count is
-  // rounded up to a multiple of 4 for register allocation: 14 / 16 warps -> 128 regs.
+  // warp roles: converters | producers | epilogue | MMA = 16 warps (128 registers).
   static constexpr int PRODUCER_WARP = CONV_WARPS;
-  static constexpr int EPI_WARP0 = CONV_WARPS + 1;
+  static constexpr int EPI_WARP0 = CONV_WARPS + PROD_WARPS;
   static constexpr int EPI_WARPS = (NP == 32) ? 4 : 8;    // 4 sub-partitions (x column halves, NP = 64)
   static constexpr int EPI_COLS = 32;                     // accumulator columns per epilogue thread
   static constexpr int MMA_WARP = EPI_WARP0 + EPI_WARPS;
@@ -68,9 +70,11 @@ struct Cfg {
   static constexpr int TMEM_COLS = 2 * N;        // double-buffered accumulator
   static constexpr int FLUSH = 2;                // tiles accumulated in TMEM (fp32) per fp64 drain
   static constexpr int SMEM_BYTES = OP_STAGES * OP_BYTES + RAW_STAGES * RAW_BYTES + 1024 /*align*/ +
-                                    (2 * OP_STAGES + 2 * RAW_STAGES + 4) * 8 /*barriers*/ + 16;
+                                    (2 * OP_STAGES + (PROD_WARPS + 1) * RAW_STAGES + 4) * 8 /*barriers*/ + 16;
+  static_assert(THREADS == 16 * 32, "16 warps");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
-  static_assert(2 * NP * (NP + 1) * 8 <= OP_STAGES * OP_BYTES, "epilogue T/B parking space");
+  // the epilogue parks T/B over the (then idle) operand + raw rings
+  static_assert(2 * NP * (NP + 1) * 8 <= OP_STAGES * OP_BYTES + RAW_STAGES * RAW_BYTES, "epilogue T/B parking space");
   static_assert(64 * 128 * 4 + 64 * 65 * 4 + 256 <= OP_STAGES * OP_BYTES, "centre-pick scratch");
   static_assert(M == 128 && KB % 32 == 0, "tile shape");
 };
@@ -238,8 +242,8 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
   unsigned char* ops = base;                                        // OP_STAGES x A operand (SW128)
   unsigned char* raw = base + C::OP_STAGES * C::OP_BYTES;           // RAW_STAGES x [NP][RAW_PITCH]
   uint64_t* bars = reinterpret_cast<uint64_t*>(raw + C::RAW_STAGES * C::RAW_BYTES);
-  uint64_t* raw_full = bars;                          // [RAW_STAGES] TMA bytes landed
-  uint64_t* raw_empty = raw_full + C::RAW_STAGES;     // [RAW_STAGES] converters done reading
+  uint64_t* raw_full = bars;                          // [RAW_STAGES][PROD_WARPS] TMA bytes landed
+  uint64_t* raw_empty = raw_full + C::RAW_STAGES * C::PROD_WARPS;   // [RAW_STAGES] converters done
   uint64_t* op_full = raw_empty + C::RAW_STAGES;      // [OP_STAGES] operand written
   uint64_t* op_free = op_full + C::OP_STAGES;         // [OP_STAGES] MMAs done reading
   uint64_t* acc_full = op_free + C::OP_STAGES;        // [2]
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::RAW_STAGES; ++s) {
-      mbar_init(&raw_full[s], 1);
+      for (int q = 0; q < C::PROD_WARPS; ++q) mbar_init(&raw_full[s * C::PROD_WARPS + q], 1);
       mbar_init(&raw_empty[s], C::CONV_WARPS);
     }
     for (int s = 0; s < C::OP_STAGES; ++s) {
@@ -277,31 +281,31 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == C::PRODUCER_WARP) {
-    // ====================================================== TMA producer
+  if (warp >= C::PRODUCER_WARP && warp < C::PRODUCER_WARP + C::PROD_WARPS) {
+    // ====================================================== TMA producers
     // One 1D bulk copy per row per raw stage (RAW_KT*4 bytes, 16-byte aligned,
-    // clamped to this CTA's range) into the raw ring, evict-first in L2.  Lane r
-    // issues row r (and r + 32).
-    const uint64_t pol = policy_evict_first();
-    const int64_t k_end = ((t0 + T) * C::KT < d) ? (t0 + T) * C::KT : d;
-    const int64_t R = (T + C::RAW_SUB - 1) / C::RAW_SUB;
-    for (int64_t j = 0; j < R; ++j) {
-      const int rs = static_cast<int>(j % C::RAW_STAGES);
-      const uint32_t use = static_cast<uint32_t>(j / C::RAW_STAGES);
-      if (use > 0) mbar_wait_sleep(&raw_empty[rs], (use - 1) & 1);
-      const int64_t k0 = t0 * C::KT + j * C::RAW_KT;
-      const int64_t cnt = (k_end - k0 < C::RAW_KT) ? k_end - k0 : C::RAW_KT;
-      const uint32_t bytes = static_cast<uint32_t>(cnt & ~int64_t(3)) * 4u;
-      if (lane == 0) mbar_arrive_expect_tx(&raw_full[rs], bytes * static_cast<uint32_t>(n));
-      __syncwarp();
-      if (bytes) {
-        unsigned char* dst = raw + rs * C::RAW_BYTES;
-#pragma unroll
-        for (int u = 0; u < NP / 32; ++u) {
-          const int r = lane + 32 * u;
-          if (r < n) {
-            if (l2_hint) bulk_g2s(dst + r * C::RAW_PITCH, rows.p[r] + k0, bytes, &raw_full[rs], pol);
-            else bulk_g2s_plain(dst + r * C::RAW_PITCH, rows.p[r] + k0, bytes, &raw_full[rs]);
+    // clamped to this CTA's range) into the raw ring.  Producer warp q issues
+    // rows r = q (mod PROD_WARPS) and arms barrier q of the stage.
+    const int q = warp - C::PRODUCER_WARP;
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const int my_rows = (n > q) ? (n - q + C::PROD_WARPS - 1) / C::PROD_WARPS : 0;
+      const int64_t k_end = ((t0 + T) * C::KT < d) ? (t0 + T) * C::KT : d;
+      const int64_t R = (T + C::RAW_SUB - 1) / C::RAW_SUB;
+      for (int64_t j = 0; j < R; ++j) {
+        const int rs = static_cast<int>(j % C::RAW_STAGES);
+        const uint32_t use = static_cast<uint32_t>(j / C::RAW_STAGES);
+        if (use > 0) mbar_wait_sleep(&raw_empty[rs], (use - 1) & 1);
+        const int64_t k0 = t0 * C::KT + j * C::RAW_KT;
+        const int64_t cnt = (k_end - k0 < C::RAW_KT) ? k_end - k0 : C::RAW_KT;
+        const uint32_t bytes = static_cast<uint32_t>(cnt & ~int64_t(3)) * 4u;
+        uint64_t* bar = &raw_full[rs * C::PROD_WARPS + q];
+        mbar_arrive_expect_tx(bar, bytes * static_cast<uint32_t>(my_rows));
+        if (bytes) {
+          unsigned char* dst = raw + rs * C::RAW_BYTES;
+          for (int r = q; r < n; r += C::PROD_WARPS) {
+            if (l2_hint) bulk_g2s(dst + r * C::RAW_PITCH, rows.p[r] + k0, bytes, bar, pol);
+            else bulk_g2s_plain(dst + r * C::RAW_PITCH, rows.p[r] + k0, bytes, bar);
           }
         }
       }
@@ -340,7 +344,9 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
     const int64_t R = (T + C::RAW_SUB - 1) / C::RAW_SUB;
     for (int64_t j = 0; j < R; ++j) {
       const int rs = static_cast<int>(j % C::RAW_STAGES);
-      mbar_wait(&raw_full[rs], static_cast<uint32_t>(j / C::RAW_STAGES) & 1);
+#pragma unroll
+      for (int q = 0; q < C::PROD_WARPS; ++q)
+        mbar_wait(&raw_full[rs * C::PROD_WARPS + q], static_cast<uint32_t>(j / C::RAW_STAGES) & 1);
 #pragma unroll
       for (int sub = 0; sub < C::RAW_SUB; ++sub) {
         const int64_t i = j * C::RAW_SUB + sub;
@@ -446,7 +452,7 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
     // park T = sum_b H_b H_b^T (TB rows 0..NP-1) and B = sum_b L_b H_b^T
     // (rows NP..2NP-1) in shared memory; blocks are added in fixed order b = 0, 1
     constexpr int EPI_THREADS = C::EPI_WARPS * 32;
-    double* TB = reinterpret_cast<double*>(ops);          // [2NP][NP+1]; operand stages are idle now
+    double* TB = reinterpret_cast<double*>(ops);          // [2NP][NP+1]; operand + raw rings are idle now
     const int tb_row = (m < C::N ? 0 : NP) + (m % NP);
     const int tb_col = (C::BLOCKS > 1) ? 0 : col0;
     named_bar(2, EPI_THREADS);
@@ -481,8 +487,8 @@ cudaError_t launch_np(const RowPtrs& rp, int n, int64_t d, double* partials, int
   const int64_t tiles = (d + C::KT - 1) / C::KT;
   int grid = num_sms < kGramMaxParts ? num_sms : kGramMaxParts;
   if (tiles < grid) grid = static_cast<int>(tiles > 0 ? tiles : 1);
-  cudaError_t e = cudaFuncSetAttribute(gram_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       C::SMEM_BYTES);
+  int occ = 0;
+  cudaError_t e = cached_occupancy(gram_tc_kernel<NP>, C::THREADS, C::SMEM_BYTES, &occ);
   if (e != cudaSuccess) return e;
   gram_tc_kernel<NP><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(rp, n, d, tiles, partials,
                                                                    l2_evict_first_enabled());

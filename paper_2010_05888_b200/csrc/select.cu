@@ -135,8 +135,8 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const double* __res
 
 cudaError_t launch_select(const double* G, int n, int f, int m, int rule, int32_t* idx_out, double* D_out,
                           cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kSelSmem));
+  int occ = 0;
+  cudaError_t e = cached_occupancy(select_kernel, kSelThreads, kSelSmem, &occ);
   if (e != cudaSuccess) return e;
   select_kernel<<<1, kSelThreads, kSelSmem, stream>>>(G, n, f, m, rule, idx_out, D_out);
   return cudaGetLastError();
