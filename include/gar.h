@@ -70,6 +70,10 @@ typedef enum {
 /* Human-readable name of a status code (static storage). */
 const char* gar_status_string(gar_status s);
 
+/* Description of the last CUDA failure (GAR_ERR_CUDA) seen by the calling
+ * thread inside libgar: cudaGetErrorString text and code; "" if none. */
+const char* gar_last_error(void);
+
 /* Bytes of device workspace gar_aggregate_ex / gar_select / gar_gram_partial
  * need for (rule, n, f, d); 0 for the coordinate-wise rules.  Pure host
  * function (no CUDA call).  Returns 0 on invalid arguments. */

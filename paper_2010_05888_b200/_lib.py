@@ -24,8 +24,8 @@ MAX_N = 64
 
 
 class GarError(RuntimeError):
-    def __init__(self, code: int, what: str):
-        super().__init__(f"{what}: {STATUS.get(code, code)}")
+    def __init__(self, code: int, what: str, detail: str = ""):
+        super().__init__(f"{what}: {STATUS.get(code, code)}" + (f" [{detail}]" if detail else ""))
         self.code = code
         self.status = STATUS.get(code, str(code))
 
@@ -40,6 +40,7 @@ def _load():
     IP = ctypes.POINTER(ctypes.c_int)
     sigs = {
         "gar_status_string": ([I], ctypes.c_char_p),
+        "gar_last_error": ([], ctypes.c_char_p),
         "gar_workspace_bytes": ([I, I, I, I64], SZ),
         "gar_num_selected": ([I, I, I, I], I),
         "gar_aggregate": ([I, PP, I, I, I64, P, P], I),
@@ -140,12 +141,17 @@ def _ptr(t):
 
 def check(code: int, what: str):
     if code != 0:
-        raise GarError(code, what)
+        detail = lib.gar_last_error().decode() if code == 7 else ""
+        raise GarError(code, what, detail)
 
 
 # ------------------------------------------------------------------ same names as the C ABI
 def gar_status_string(code: int) -> str:
     return lib.gar_status_string(code).decode()
+
+
+def gar_last_error() -> str:
+    return lib.gar_last_error().decode()
 
 
 def gar_workspace_bytes(rule, n: int, f: int, d: int) -> int:

@@ -87,20 +87,22 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // fminf(NaN, +inf) = +inf (min returns the non-NaN operand); x + 0 maps -0 to +0.
 __device__ __forceinline__ float canon(float v) { return __fadd_rn(fminf(v, __int_as_float(0x7f800000)), 0.0f); }
 
-// Host helper: set the dynamic shared-memory limit of `kern` and query its
-// occupancy once per (kernel, device, smem size); both calls cost microseconds,
-// which dominate small aggregations.
+// Host helper: query (and cache) the occupancy of `kern` at (threads, smem).
+// The dynamic shared-memory limit is a per-FUNCTION attribute shared by every
+// launch configuration of that kernel, so it is raised once per (kernel,
+// device) to the device's opt-in maximum rather than to one configuration's
+// size (a smaller configuration would otherwise lower it under a larger one).
+// Both CUDA calls cost microseconds, which dominate small aggregations.
 template <class K>
 inline cudaError_t cached_occupancy(K kern, int threads, size_t smem, int* occ) {
-  // keyed by the kernel's address: instantiations of one template share the type K
   struct Entry {
     const void* fn = nullptr;
     int device = -1;
-    int threads = 0;
+    int threads = 0;       // 0: the "attribute raised" marker entry
     size_t smem = 0;
     int occ = 0;
   };
-  static Entry cache[64];
+  static Entry cache[128];
   static int next = 0;
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
@@ -108,24 +110,36 @@ inline cudaError_t cached_occupancy(K kern, int threads, size_t smem, int* occ) 
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   const void* fn = reinterpret_cast<const void*>(kern);
-  for (const Entry& c : cache)
-    if (c.fn == fn && c.device == dev && c.threads == threads && c.smem == smem) {
+  bool raised = false;
+  for (const Entry& c : cache) {
+    if (c.fn != fn || c.device != dev) continue;
+    if (c.threads == 0) raised = true;
+    if (c.threads == threads && c.smem == smem) {
       *occ = c.occ;
       return cudaSuccess;
     }
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
+  }
+  if (!raised) {
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    int optin = 0;
+    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - static_cast<int>(fa.sharedSizeBytes));
+    if (e != cudaSuccess) return e;
+    Entry& m = cache[next];
+    next = (next + 1) % 128;
+    m = Entry{fn, dev, 0, 0, 0};
+  }
   int o = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem);
   if (e != cudaSuccess) return e;
   o = o > 0 ? o : 1;
   Entry& c = cache[next];
-  next = (next + 1) % 64;
-  c.fn = fn;
-  c.device = dev;
-  c.threads = threads;
-  c.smem = smem;
-  c.occ = o;
+  next = (next + 1) % 128;
+  c = Entry{fn, dev, threads, smem, o};
   *occ = o;
   return cudaSuccess;
 }

@@ -3,6 +3,7 @@
 // host; every step runs in the kernels of coord_select*.cu, gram_*.cu and
 // select.cu.
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <cuda_runtime.h>
 
@@ -68,13 +69,25 @@ gar_status check_out(const float* const* grads, int n, int64_t d, const float* o
   return GAR_OK;
 }
 
+thread_local char g_last_error[256] = "";
+
+inline gar_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return GAR_OK;
+  std::snprintf(g_last_error, sizeof(g_last_error), "%s (%d)", cudaGetErrorString(e), static_cast<int>(e));
+  cudaGetLastError();   // clear non-sticky errors so the next call starts clean
+  return GAR_ERR_CUDA;
+}
+
 // Device-pointer check (no CPU fallback: host memory is rejected).
 gar_status check_device_ptr(const void* p) {
   cudaPointerAttributes a;
   cudaError_t e = cudaPointerGetAttributes(&a, p);
   if (e != cudaSuccess) {
-    cudaGetLastError();
-    return e == cudaErrorInvalidValue ? GAR_ERR_INVALID_ARGUMENT : GAR_ERR_CUDA;
+    if (e == cudaErrorInvalidValue) {
+      cudaGetLastError();
+      return GAR_ERR_INVALID_ARGUMENT;
+    }
+    return cuda_status(e);
   }
   if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return GAR_ERR_INVALID_ARGUMENT;
   return GAR_OK;
@@ -156,12 +169,10 @@ Workspace carve(void* ws, int n) {
   return w;
 }
 
-inline gar_status cuda_status(cudaError_t e) { return e == cudaSuccess ? GAR_OK : GAR_ERR_CUDA; }
-
 gar_status run_gram(const float* const* grads, int n, int64_t d, const Workspace& w, cudaStream_t st) {
   int parts = 0;
-  cudaError_t e = gar::launch_gram_partials(grads, n, d, w.partials, num_sms(), &parts, st);
-  if (e != cudaSuccess) return GAR_ERR_CUDA;
+  gar_status s = cuda_status(gar::launch_gram_partials(grads, n, d, w.partials, num_sms(), &parts, st));
+  if (s != GAR_OK) return s;
   return cuda_status(gar::launch_gram_reduce(w.partials, parts, n, w.G, st));
 }
 
@@ -192,6 +203,8 @@ gar_status run_combine(gar_rule rule, const float* const* grads, int n, int f, i
 }  // namespace
 
 extern "C" {
+
+const char* gar_last_error(void) { return g_last_error; }
 
 const char* gar_status_string(gar_status s) {
   switch (s) {
@@ -262,11 +275,12 @@ gar_status gar_aggregate(gar_rule rule, const float* const* grads, int n, int f,
   void* ws = nullptr;
   const size_t bytes = gar_workspace_bytes(rule, n, f, d);
   if (bytes) {
-    if (cudaMallocAsync(&ws, bytes, st) != cudaSuccess) return GAR_ERR_CUDA;
+    if ((s = cuda_status(cudaMallocAsync(&ws, bytes, st))) != GAR_OK) return s;
   }
   s = gar_aggregate_ex(rule, grads, n, f, 0, d, out, nullptr, ws, bytes, stream);
   if (ws) {
-    if (cudaFreeAsync(ws, st) != cudaSuccess && s == GAR_OK) s = GAR_ERR_CUDA;
+    const gar_status f = cuda_status(cudaFreeAsync(ws, st));
+    if (s == GAR_OK) s = f;
   }
   return s;
 }
@@ -316,8 +330,8 @@ gar_status gar_gram_partial(const float* const* grads, int n, int64_t d_local, d
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Workspace w = carve(workspace, n);
   int parts = 0;
-  if (gar::launch_gram_partials(grads, n, d_local, w.partials, num_sms(), &parts, st) != cudaSuccess)
-    return GAR_ERR_CUDA;
+  if ((s = cuda_status(gar::launch_gram_partials(grads, n, d_local, w.partials, num_sms(), &parts, st))) != GAR_OK)
+    return s;
   return cuda_status(gar::launch_gram_reduce(w.partials, parts, n, gram_dev, st));
 }
 

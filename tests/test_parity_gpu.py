@@ -213,3 +213,18 @@ def test_errors_from_python(gar):
         _lib.check(_lib.lib.gar_aggregate_ex(1, arr, n, 1, 0, 16, ctypes.c_void_p(host.data_ptr()), None, None, 0,
                                              None), "host out")
     assert e.value.code == 1
+
+
+def test_interleaved_launch_configurations(gar):
+    """One kernel launched with different shared-memory sizes in turn (Average
+    over 31 rows, Multi-Krum's combine over 22, ...): the per-function
+    dynamic shared-memory limit must never be left below a later launch's need."""
+    n, f, d = 31, 7, 120_001
+    x = synth.make_gradients(n, f, d, seed=123, ld=d).numpy()
+    X = to_device(x)
+    ref_avg = oracle.average(x)
+    for _ in range(2):
+        for rule in ("average", "multi_krum", "average", "bulyan", "trimmed_mean", "average", "krum", "median"):
+            out, sel = run_rule(gar, rule, X, d, f)
+            if rule == "average":
+                assert_same_bits(out, ref_avg, rule)
