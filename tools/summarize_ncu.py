@@ -32,7 +32,7 @@ KEYS = {
 def kclass(name):
     if "gram_tc" in name:
         return "gram"
-    if "coord_select" in name or "copy_row" in name:
+    if "coord_select" in name or "coord_ldg" in name or "copy_row" in name:
         return "coord_select"
     if "select_kernel" in name:
         return "select"
