@@ -45,8 +45,9 @@ def parse():
     ap.add_argument("--workload", default="C3", help="C1..C4 or sweep:<n>")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--output", default="replicated", choices=["replicated", "sharded"],
-                    help="N>1: all-gather the aggregate to every rank (north_star) or keep it d-sharded")
+    ap.add_argument("--output", default="fused", choices=["replicated", "sharded", "fused"],
+                    help="N>1: all-gather the aggregate to every rank with NCCL (north_star), write it into every "
+                         "rank's buffer from the producing kernel over NVLink (fused), or keep it d-sharded")
     return ap.parse_args()
 
 
@@ -231,7 +232,8 @@ def run_ours(args):
             X.copy_(host_x, non_blocking=True)
             for r in RULES:
                 res = aggs[r].aggregate(X, out_local=outs[r], out_full=full[r])
-                host_out[r].copy_(res[:dl] if world == 1 else outs[r], non_blocking=True)
+                local_res = res[lo:hi] if res.numel() > dl else res
+                host_out[r].copy_(local_res, non_blocking=True)
         b = ev()
         torch.cuda.synchronize()
         e2e_ms = a.elapsed_time(b) / args.e2e_steps

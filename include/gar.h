@@ -138,6 +138,25 @@ gar_status gar_combine(gar_rule rule, const float* const* grads, int n, int f, i
                        int64_t d_local, const int32_t* indices_dev, float* out,
                        gar_stream_t stream);
 
+/* ---- fused output all-gather (multi-GPU) ----------------------
+ * As gar_aggregate_ex / gar_combine, but every result coordinate is ALSO
+ * stored at extra_outs[j][i] (j < n_extra <= 8) by the producing kernel itself.
+ * For a d-sharded rank, extra_outs[j] is the position of this rank's slice in
+ * GPU j's replicated output buffer, mapped into this GPU's address space
+ * (e.g. torch symmetric memory): the all-gather of the aggregate then travels
+ * over NVLink inside the kernel that computes it instead of in a separate
+ * collective.  The caller synchronises the ranks before reading (barrier).
+ * extra_outs: host array of device or peer-mapped pointers, 16-byte aligned,
+ * not aliasing the inputs; they are not checked for host memory. */
+gar_status gar_aggregate_bcast(gar_rule rule, const float* const* grads, int n, int f, int m,
+                               int64_t d, float* out, float* const* extra_outs, int n_extra,
+                               int32_t* indices_dev, void* workspace, size_t workspace_bytes,
+                               gar_stream_t stream);
+
+gar_status gar_combine_bcast(gar_rule rule, const float* const* grads, int n, int f, int m,
+                             int64_t d_local, const int32_t* indices_dev, float* out,
+                             float* const* extra_outs, int n_extra, gar_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -50,6 +50,8 @@ def _load():
         "gar_gram_partial": ([PP, I, I64, P, P, SZ, P], I),
         "gar_select_from_gram": ([I, P, I, I, I, P, IP, P, SZ, P], I),
         "gar_combine": ([I, PP, I, I, I, I64, P, P, P], I),
+        "gar_aggregate_bcast": ([I, PP, I, I, I, I64, P, PP, I, P, P, SZ, P], I),
+        "gar_combine_bcast": ([I, PP, I, I, I, I64, P, P, PP, I, P], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -216,4 +218,30 @@ def gar_combine(rule, grads, f: int, m: int, indices: torch.Tensor, out: torch.T
     arr, n, d, dev = row_pointers(grads, d)
     check(lib.gar_combine(rule_id(rule), arr, n, f, m, d, _ptr(indices), _ptr(out),
                           stream_handle(dev, stream)), "gar_combine")
+    return out
+
+
+def _ptr_array(addrs):
+    addrs = list(addrs)
+    return (ctypes.c_void_p * max(len(addrs), 1))(*addrs), len(addrs)
+
+
+def gar_aggregate_bcast(rule, grads, f: int, m: int, out: torch.Tensor, extra_ptrs, indices=None, workspace=None,
+                        d: int | None = None, stream=None):
+    """gar_aggregate_ex + the result also stored at each address of extra_ptrs
+    (ints: peer-mapped buffers, e.g. torch symmetric memory)."""
+    arr, n, d, dev = row_pointers(grads, d)
+    ex, ne = _ptr_array(extra_ptrs)
+    wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    check(lib.gar_aggregate_bcast(rule_id(rule), arr, n, f, m, d, _ptr(out), ex, ne, _ptr(indices), _ptr(workspace),
+                                  wsb, stream_handle(dev, stream)), "gar_aggregate_bcast")
+    return out
+
+
+def gar_combine_bcast(rule, grads, f: int, m: int, indices: torch.Tensor, out: torch.Tensor, extra_ptrs,
+                      d: int | None = None, stream=None):
+    arr, n, d, dev = row_pointers(grads, d)
+    ex, ne = _ptr_array(extra_ptrs)
+    check(lib.gar_combine_bcast(rule_id(rule), arr, n, f, m, d, _ptr(indices), _ptr(out), ex, ne,
+                                stream_handle(dev, stream)), "gar_combine_bcast")
     return out

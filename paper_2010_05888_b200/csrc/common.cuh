@@ -14,6 +14,22 @@ struct RowPtrs {
   const float* p[GAR_MAX_N];
 };
 
+// Extra output destinations (fused output all-gather): every
+// result is also stored at p[j][i] for j < n -- the same offset in the other
+// GPUs' replicated output buffers, mapped into this GPU's address space
+// (symmetric memory), so the stores travel over NVLink inside the producing
+// kernel instead of in a separate all-gather.
+#define GAR_MAX_PEERS 8
+struct OutPtrs {
+  float* p[GAR_MAX_PEERS];
+  int n;
+};
+
+__device__ __forceinline__ void store_result(float* out, const OutPtrs& extra, int64_t i, float v) {
+  __stcs(out + i, v);
+  for (int j = 0; j < extra.n; ++j) extra.p[j][i] = v;
+}
+
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

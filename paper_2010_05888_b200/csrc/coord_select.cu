@@ -10,16 +10,18 @@ namespace gar {
 // Krum combine (one selected row): out = fp32((0 + x) / 1) = x + 0 (-0 -> +0),
 // a plain vectorised streaming copy.
 __global__ void __launch_bounds__(256) copy_row_kernel(const __grid_constant__ RowPtrs rows, const int32_t* idx,
-                                                        float* __restrict__ out, int64_t d) {
+                                                        float* __restrict__ out, const __grid_constant__ OutPtrs extra,
+                                                        int64_t d) {
   const float* src = rows.p[idx ? idx[0] : 0];
   const int64_t n4 = d >> 2;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n4; q += int64_t(gridDim.x) * blockDim.x) {
     float4 v = __ldcs(reinterpret_cast<const float4*>(src) + q);
     v.x = __fadd_rn(v.x, 0.0f); v.y = __fadd_rn(v.y, 0.0f); v.z = __fadd_rn(v.z, 0.0f); v.w = __fadd_rn(v.w, 0.0f);
     __stcs(reinterpret_cast<float4*>(out) + q, v);
+    for (int j = 0; j < extra.n; ++j) reinterpret_cast<float4*>(extra.p[j])[q] = v;
   }
   const int64_t k = (n4 << 2) + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (blockIdx.x == 0 && k < d) out[k] = __fadd_rn(src[k], 0.0f);
+  if (blockIdx.x == 0 && k < d) store_result(out, extra, k, __fadd_rn(src[k], 0.0f));
 }
 
 int l2_evict_first_enabled() {
@@ -49,7 +51,7 @@ inline cudaError_t launch_copy_row(const CoordLaunch& L, cudaStream_t stream) {
   const int64_t cap = int64_t(L.num_sms) * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  copy_row_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(rp, L.idx, L.out, L.d);
+  copy_row_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(rp, L.idx, L.out, L.extra, L.d);
   return cudaGetLastError();
 }
 

@@ -3,6 +3,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "common.cuh"
+
 namespace gar {
 
 enum CoordMode { kModeAverage = 0, kModeMedian = 1, kModeTrimmed = 2, kModeBulyan = 3 };
@@ -15,6 +17,7 @@ struct CoordLaunch {
   int f;                      // trim per side / Bulyan f
   int64_t d;                  // coordinates
   float* out;                 // device fp32[d]
+  OutPtrs extra;              // further destinations (n = 0: none)
   int num_sms;
 };
 

@@ -38,6 +38,7 @@ struct CoordParams {
   RowPtrs rows;
   const int32_t* idx;   // nullptr: rows 0..R-1; else R selected input indices
   float* out;
+  OutPtrs extra;        // further destinations of every result (peer GPUs' buffers)
   int64_t d;
   int R;                // rows consumed per coordinate
   int f;                // trimmed mean: trim per side; Bulyan: declared f
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(32 * (W + kProducers), 1) coord_select_kernel(
           res = bulyan_column<N>(v, col, kTile, p.f, rowp, start + c);
         }
       }
-      p.out[start + c] = res;
+      store_result(p.out, p.extra, start + c, res);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
@@ -311,7 +312,7 @@ __global__ void __launch_bounds__(kLdgThreads) coord_ldg_kernel(const __grid_con
         res = bulyan_column<N>(v, col, kLdgThreads, p.f, rowp, k);
       }
     }
-    __stcs(p.out + k, res);
+    store_result(p.out, p.extra, k, res);
   }
 }
 
@@ -321,6 +322,7 @@ inline cudaError_t launch_ldg(const CoordLaunch& L, cudaStream_t stream) {
   for (int i = 0; i < GAR_MAX_N; ++i) p.rows.p[i] = (i < L.n) ? L.rows[i] : nullptr;
   p.idx = L.idx;
   p.out = L.out;
+  p.extra = L.extra;
   p.d = L.d;
   p.R = L.R;
   p.f = L.f;
@@ -356,6 +358,7 @@ inline cudaError_t launch_mode_w(const CoordLaunch& L, cudaStream_t stream) {
   for (int i = 0; i < GAR_MAX_N; ++i) p.rows.p[i] = (i < L.n) ? L.rows[i] : nullptr;
   p.idx = L.idx;
   p.out = L.out;
+  p.extra = L.extra;
   p.d = L.d;
   p.R = L.R;
   p.f = L.f;

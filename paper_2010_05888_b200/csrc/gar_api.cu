@@ -183,7 +183,7 @@ gar_status run_select(gar_rule rule, const double* G, int n, int f, int me, int3
 }
 
 gar_status run_combine(gar_rule rule, const float* const* grads, int n, int f, int me, int64_t d,
-                       const int32_t* idx, float* out, cudaStream_t st) {
+                       const int32_t* idx, float* out, const gar::OutPtrs& extra, cudaStream_t st) {
   CoordLaunch L{};
   L.rows = grads;
   L.n = n;
@@ -191,6 +191,7 @@ gar_status run_combine(gar_rule rule, const float* const* grads, int n, int f, i
   L.f = f;
   L.d = d;
   L.out = out;
+  L.extra = extra;
   L.num_sms = num_sms();
   if (rule == GAR_BULYAN) {
     L.R = n - 2 * f;
@@ -198,6 +199,70 @@ gar_status run_combine(gar_rule rule, const float* const* grads, int n, int f, i
   }
   L.R = me;
   return cuda_status(gar::launch_coord_select(gar::kModeAverage, L, st));
+}
+
+// Extra destinations of the broadcast variants: non-null, 16-byte aligned, at
+// most GAR_MAX_PEERS; they may be peer-mapped (symmetric) memory, so they are
+// not checked with cudaPointerGetAttributes.
+gar_status make_extra(float* const* extra_outs, int n_extra, gar::OutPtrs* extra) {
+  extra->n = 0;
+  if (n_extra < 0 || n_extra > GAR_MAX_PEERS || (n_extra > 0 && !extra_outs)) return GAR_ERR_INVALID_ARGUMENT;
+  for (int j = 0; j < n_extra; ++j) {
+    if (!extra_outs[j]) return GAR_ERR_INVALID_ARGUMENT;
+    if (reinterpret_cast<uintptr_t>(extra_outs[j]) & 15u) return GAR_ERR_ALIGNMENT;
+    extra->p[j] = extra_outs[j];
+  }
+  extra->n = n_extra;
+  return GAR_OK;
+}
+
+gar_status aggregate_impl(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d, float* out,
+                          const gar::OutPtrs& extra, int32_t* indices_dev, void* workspace, size_t workspace_bytes,
+                          gar_stream_t stream) {
+  gar_status s = check_rule_args(rule, n, f, m);
+  if (s != GAR_OK) return s;
+  if ((s = check_rows(grads, n, d)) != GAR_OK) return s;
+  if ((s = check_out(grads, n, d, out)) != GAR_OK) return s;
+  const bool krum = is_krum_family(rule);
+  if (krum && (!workspace || workspace_bytes < ws_bytes_for(n))) return GAR_ERR_WORKSPACE;
+  if ((s = check_device_rows(grads, n, out)) != GAR_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+
+  if (!krum) {
+    CoordLaunch L{};
+    L.rows = grads;
+    L.n = n;
+    L.idx = nullptr;
+    L.R = n;
+    L.f = f;
+    L.d = d;
+    L.out = out;
+    L.extra = extra;
+    L.num_sms = num_sms();
+    int mode = gar::kModeAverage;
+    if (rule == GAR_MEDIAN) mode = gar::kModeMedian;
+    if (rule == GAR_TRIMMED_MEAN) mode = gar::kModeTrimmed;
+    return cuda_status(gar::launch_coord_select(mode, L, st));
+  }
+  const int me = effective_m(rule, n, f, m);
+  Workspace w = carve(workspace, n);
+  int32_t* idx = indices_dev ? indices_dev : w.idx;
+  if ((s = run_gram(grads, n, d, w, st)) != GAR_OK) return s;
+  if ((s = run_select(rule, w.G, n, f, me, idx, nullptr, st)) != GAR_OK) return s;
+  return run_combine(rule, grads, n, f, me, d, idx, out, extra, st);
+}
+
+gar_status combine_impl(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d_local,
+                        const int32_t* indices_dev, float* out, const gar::OutPtrs& extra, gar_stream_t stream) {
+  gar_status s = check_rule_args(rule, n, f, m);
+  if (s != GAR_OK) return s;
+  if (!is_krum_family(rule)) return GAR_ERR_UNSUPPORTED;
+  if (!indices_dev) return GAR_ERR_INVALID_ARGUMENT;
+  if ((s = check_rows(grads, n, d_local)) != GAR_OK) return s;
+  if ((s = check_out(grads, n, d_local, out)) != GAR_OK) return s;
+  if ((s = check_device_rows(grads, n, out)) != GAR_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return run_combine(rule, grads, n, f, effective_m(rule, n, f, m), d_local, indices_dev, out, extra, st);
 }
 
 }  // namespace
@@ -235,36 +300,17 @@ int gar_num_selected(gar_rule rule, int n, int f, int m) {
 gar_status gar_aggregate_ex(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d,
                             float* out, int32_t* indices_dev, void* workspace, size_t workspace_bytes,
                             gar_stream_t stream) {
-  gar_status s = check_rule_args(rule, n, f, m);
-  if (s != GAR_OK) return s;
-  if ((s = check_rows(grads, n, d)) != GAR_OK) return s;
-  if ((s = check_out(grads, n, d, out)) != GAR_OK) return s;
-  const bool krum = is_krum_family(rule);
-  if (krum && (!workspace || workspace_bytes < ws_bytes_for(n))) return GAR_ERR_WORKSPACE;
-  if ((s = check_device_rows(grads, n, out)) != GAR_OK) return s;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  gar::OutPtrs none{};
+  return aggregate_impl(rule, grads, n, f, m, d, out, none, indices_dev, workspace, workspace_bytes, stream);
+}
 
-  if (!krum) {
-    CoordLaunch L{};
-    L.rows = grads;
-    L.n = n;
-    L.idx = nullptr;
-    L.R = n;
-    L.f = f;
-    L.d = d;
-    L.out = out;
-    L.num_sms = num_sms();
-    int mode = gar::kModeAverage;
-    if (rule == GAR_MEDIAN) mode = gar::kModeMedian;
-    if (rule == GAR_TRIMMED_MEAN) mode = gar::kModeTrimmed;
-    return cuda_status(gar::launch_coord_select(mode, L, st));
-  }
-  const int me = effective_m(rule, n, f, m);
-  Workspace w = carve(workspace, n);
-  int32_t* idx = indices_dev ? indices_dev : w.idx;
-  if ((s = run_gram(grads, n, d, w, st)) != GAR_OK) return s;
-  if ((s = run_select(rule, w.G, n, f, me, idx, nullptr, st)) != GAR_OK) return s;
-  return run_combine(rule, grads, n, f, me, d, idx, out, st);
+gar_status gar_aggregate_bcast(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d,
+                               float* out, float* const* extra_outs, int n_extra, int32_t* indices_dev,
+                               void* workspace, size_t workspace_bytes, gar_stream_t stream) {
+  gar::OutPtrs extra{};
+  gar_status s = make_extra(extra_outs, n_extra, &extra);
+  if (s != GAR_OK) return s;
+  return aggregate_impl(rule, grads, n, f, m, d, out, extra, indices_dev, workspace, workspace_bytes, stream);
 }
 
 gar_status gar_aggregate(gar_rule rule, const float* const* grads, int n, int f, int64_t d, float* out,
@@ -355,15 +401,17 @@ gar_status gar_select_from_gram(gar_rule rule, const double* gram_dev, int n, in
 
 gar_status gar_combine(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d_local,
                        const int32_t* indices_dev, float* out, gar_stream_t stream) {
-  gar_status s = check_rule_args(rule, n, f, m);
+  gar::OutPtrs none{};
+  return combine_impl(rule, grads, n, f, m, d_local, indices_dev, out, none, stream);
+}
+
+gar_status gar_combine_bcast(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d_local,
+                             const int32_t* indices_dev, float* out, float* const* extra_outs, int n_extra,
+                             gar_stream_t stream) {
+  gar::OutPtrs extra{};
+  gar_status s = make_extra(extra_outs, n_extra, &extra);
   if (s != GAR_OK) return s;
-  if (!is_krum_family(rule)) return GAR_ERR_UNSUPPORTED;
-  if (!indices_dev) return GAR_ERR_INVALID_ARGUMENT;
-  if ((s = check_rows(grads, n, d_local)) != GAR_OK) return s;
-  if ((s = check_out(grads, n, d_local, out)) != GAR_OK) return s;
-  if ((s = check_device_rows(grads, n, out)) != GAR_OK) return s;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  return run_combine(rule, grads, n, f, effective_m(rule, n, f, m), d_local, indices_dev, out, st);
+  return combine_impl(rule, grads, n, f, m, d_local, indices_dev, out, extra, stream);
 }
 
 }  // extern "C"

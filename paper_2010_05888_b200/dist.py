@@ -14,9 +14,11 @@ coordinates).  Then:
   disjoint slices add up exactly), every rank runs the identical deterministic
   selection (``gar_select_from_gram``) and combines its own slice
   (``gar_combine``);
-* the aggregate is all-gathered (``output="replicated"``, the north_star
-  default) or left d-sharded (``output="sharded"``, what a ZeRO-style
-  optimizer consumes).
+* the aggregate is all-gathered (``output="replicated"``: NCCL all-gather
+  after the kernel, the north_star default), written by the producing kernel
+  itself into every GPU's output buffer over NVLink (``output="fused"``:
+  torch symmetric memory, ``gar_*_bcast``; one device-side barrier), or left
+  d-sharded (``output="sharded"``, what a ZeRO-style optimizer consumes).
 
 The paper's own exchange is PyTorch ``broadcast``/``gather`` over NCCL or gloo
 (§4.2); here the only collectives are one tiny
@@ -63,8 +65,14 @@ class _LibgarBackend:
     def select_from_gram(self, rule, gram, n, f, m, idx):
         return self._lib.gar_select_from_gram(rule, gram, n, f, m, idx)
 
-    def combine(self, rule, rows, f, m, idx, out, d):
-        self._lib.gar_combine(rule, rows, f, m, idx, out, d=d)
+    def combine(self, rule, rows, f, m, idx, out, d, extra=()):
+        if extra:
+            self._lib.gar_combine_bcast(rule, rows, f, m, idx, out, extra, d=d)
+        else:
+            self._lib.gar_combine(rule, rows, f, m, idx, out, d=d)
+
+    def coordinatewise_bcast(self, agg, rows, out, d, extra):
+        self._lib.gar_aggregate_bcast(agg.rule, rows, agg.f, agg.m, out, extra, workspace=None, d=d)
 
 
 class ShardedAggregator:
@@ -73,7 +81,7 @@ class ShardedAggregator:
 
     def __init__(self, rule: str, n: int, f: int, d: int, m: int | None = None, group=None,
                  output: str = "replicated", backend=None):
-        if output not in ("replicated", "sharded"):
+        if output not in ("replicated", "sharded", "fused"):
             raise ValueError(output)
         self.rule, self.n, self.f, self.d = rule, int(n), int(f), int(d)
         self.m = 0 if m is None else int(m)
@@ -90,6 +98,19 @@ class ShardedAggregator:
         self._gram = None
         self._idx = None
         self._pad = None
+        self._symm = None          # (symmetric out_full, handle, extra peer addresses) for output="fused"
+
+    def _fused_buffers(self, device):
+        """Replicated output in symmetric memory; the addresses of this rank's
+        slice in every OTHER rank's buffer (peer-mapped over NVLink)."""
+        if self._symm is None:
+            import torch.distributed._symmetric_memory as symm_mem
+            buf = symm_mem.empty(self.per * self.world, dtype=torch.float32, device=device)
+            group = self.group if self.group is not None else dist.group.WORLD
+            handle = symm_mem.rendezvous(buf, group)
+            extra = [int(handle.buffer_ptrs[r]) + 4 * self.lo for r in range(self.world) if r != self.rank]
+            self._symm = (buf, handle, extra)
+        return self._symm
 
     # -- lazily created per-device state ------------------------------------------
     def _state(self, device):
@@ -115,6 +136,8 @@ class ShardedAggregator:
         dev = rows_local.device if isinstance(rows_local, torch.Tensor) else rows_local[0].device
         self._state(dev)
         mark = mark or (lambda label: None)
+        if self.output == "fused" and self.world > 1:
+            return self._aggregate_fused(rows_local, dev, mark)
         if out_local is None:
             out_local = torch.empty(self.d_local, dtype=torch.float32, device=dev)
         if self.rule in KRUM_FAMILY:
@@ -143,6 +166,25 @@ class ShardedAggregator:
             dist.all_gather_into_tensor(out_full, self._pad, group=self.group)
         mark("gather")
         return out_full[: self.d]
+
+    def _aggregate_fused(self, rows_local, dev, mark):
+        buf, handle, extra = self._fused_buffers(dev)
+        out_local = buf[self.lo: self.hi]
+        if self.rule in KRUM_FAMILY:
+            self.backend.gram_partial(rows_local, self._gram, self._ws, self.d_local)
+            mark("gram")
+            dist.all_reduce(self._gram, op=dist.ReduceOp.SUM, group=self.group)
+            mark("exchange")
+            self.backend.select_from_gram(self.rule, self._gram, self.n, self.f, self.m, self._idx)
+            mark("select")
+            self.backend.combine(self.rule, rows_local, self.f, self.m, self._idx, out_local, self.d_local, extra)
+            mark("combine")
+        else:
+            self.backend.coordinatewise_bcast(self._agg, rows_local, out_local, self.d_local, extra)
+            mark("coord")
+        handle.barrier()        # every rank's slices have landed in every buffer
+        mark("gather")
+        return buf[: self.d]
 
     @property
     def selected(self) -> torch.Tensor | None:

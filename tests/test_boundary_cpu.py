@@ -124,3 +124,21 @@ def test_networks_header_is_reproducible(tmp_path):
     out = tmp_path / "networks.cuh"
     subprocess.check_call([sys.executable, gen, str(out)])
     assert filecmp.cmp(out, os.path.join(ROOT, "paper_2010_05888_b200", "csrc", "networks.cuh"), shallow=False)
+
+
+def test_bcast_entry_points_check_their_extra_outputs(gl):
+    n = 5
+    ptrs = (ctypes.c_void_p * n)(*[0x20_0000 + 0x1000 * i for i in range(n)])
+    def agg(extra, n_extra):
+        arr = (ctypes.c_void_p * max(len(extra), 1))(*extra)
+        return gl.lib.gar_aggregate_bcast(gl.rule_id("median"), ptrs, n, 1, 0, 100, ctypes.c_void_p(0x10_0000),
+                                          arr, n_extra, None, None, 0, None)
+    assert agg([0x40_0000 + 4], 1) == 4            # misaligned extra destination
+    assert agg([0], 1) == 1                        # null extra destination
+    assert agg([0x40_0000] * 9, 9) == 1            # more than GAR_MAX_PEERS
+    assert agg([0x40_0000], -1) == 1
+    assert agg([0x40_0000], 1) in (1, 7)           # valid: reaches the device check (no GPU here)
+    arr = (ctypes.c_void_p * 1)(0x40_0000)
+    code = gl.lib.gar_combine_bcast(gl.rule_id("median"), ptrs, n, 1, 0, 100, ctypes.c_void_p(0x1000),
+                                    ctypes.c_void_p(0x10_0000), arr, 1, None)
+    assert code == 5                               # combine is for the Krum family
