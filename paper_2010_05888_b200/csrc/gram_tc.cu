@@ -33,19 +33,20 @@ namespace {
 
 template <int NP_>
 struct Cfg {
-  static constexpr int NP = NP_;                 // padded row count (32 or 64)
+  static constexpr int NP = NP_;                 // padded row count (16, 32 or 64)
   // Block-diagonal packing: a tile's coordinates are split into BLOCKS blocks
   // that share the MMA's K index; A = [H_0..H_{B-1}; L_0..L_{B-1}] and
   // B = [H_0..H_{B-1}], so the diagonal blocks of D = A B^T are the useful
   // H_b H_b^T and L_b H_b^T (off-diagonal blocks pair different coordinates
   // and are ignored).  NP = 32 -> 2 blocks, M = 128, N = 64: half the MMA
   // instructions of M = 64, N = 32 and the full 128-lane datapath.
-  static constexpr int BLOCKS = 64 / NP;         // 2 / 1
+  static constexpr int BLOCKS = 64 / NP;         // 4 / 2 / 1
   static constexpr int M = 2 * NP * BLOCKS;      // 128: H rows of all blocks, then L rows
   static constexpr int N = NP * BLOCKS;          // 64: H rows of all blocks
-  static constexpr int CONV_WARPS = (NP == 32) ? 8 : 4;   // converters: 16 coordinates each
-  static constexpr int KT = 16 * CONV_WARPS;     // coordinates per tile: 128 / 64
-  static constexpr int KB = KT / BLOCKS;         // coordinates per block (MMA K extent): 64 / 64
+  static constexpr int CONV_WARPS = (NP <= 32) ? 8 : 4;   // converters: 16*CH coordinates each
+  static constexpr int CH = (NP == 16) ? 2 : 1;  // float4 chunks per lane per tile (per-tile costs vs rows)
+  static constexpr int KT = 16 * CH * CONV_WARPS;     // coordinates per tile: 256 / 128 / 64
+  static constexpr int KB = KT / BLOCKS;         // coordinates per block (MMA K extent): 64 / 64 / 64
   static constexpr int ATOMS = KB / 32;          // 128-byte K atoms per tile
   static constexpr int ATOM_BYTES = M * 128;     // one K atom of A (8-row groups of 1 KB)
   static constexpr int OP_BYTES = ATOMS * ATOM_BYTES;      // one operand stage (A; B aliases its H rows)
@@ -55,15 +56,15 @@ struct Cfg {
   // each): bulk-copy issue is limited per request and per issuing warp
   // (tools/membench.cu, membench2.cu).
   static constexpr int PROD_WARPS = 3;
-  static constexpr int RAW_SUB = (NP == 32) ? 3 : 4;
+  static constexpr int RAW_SUB = (NP == 16) ? 2 : (NP == 32) ? 3 : 4;   // 2 KB / 1.5 KB / 1 KB per row
   static constexpr int RAW_KT = RAW_SUB * KT;    // coordinates per raw stage
   static constexpr int RAW_PITCH = RAW_KT * 4 + 16;   // bytes per raw row (+16: conflict-free LDS.128)
   static constexpr int RAW_BYTES = NP * RAW_PITCH;    // one raw stage (TMA destination)
-  static constexpr int RAW_STAGES = (NP == 32) ? 3 : 2;   // ~96 KB / ~50 KB in flight while one drains
+  static constexpr int RAW_STAGES = (NP == 16) ? 4 : (NP == 32) ? 3 : 2;
   // warp roles: converters | producers | epilogue | MMA = 16 warps (128 registers).
   static constexpr int PRODUCER_WARP = CONV_WARPS;
   static constexpr int EPI_WARP0 = CONV_WARPS + PROD_WARPS;
-  static constexpr int EPI_WARPS = (NP == 32) ? 4 : 8;    // 4 sub-partitions (x column halves, NP = 64)
+  static constexpr int EPI_WARPS = (NP <= 32) ? 4 : 8;    // 4 sub-partitions (x column halves, NP = 64)
   static constexpr int EPI_COLS = 32;                     // accumulator columns per epilogue thread
   static constexpr int MMA_WARP = EPI_WARP0 + EPI_WARPS;
   static constexpr int THREADS = (MMA_WARP + 1) * 32;
@@ -75,7 +76,7 @@ struct Cfg {
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   // the epilogue parks T/B over the (then idle) operand + raw rings
   static_assert(2 * NP * (NP + 1) * 8 <= OP_STAGES * OP_BYTES + RAW_STAGES * RAW_BYTES, "epilogue T/B parking space");
-  static_assert(64 * 128 * 4 + 64 * 65 * 4 + 256 <= OP_STAGES * OP_BYTES, "centre-pick scratch");
+  static_assert(NP * 128 * 4 + NP * (NP + 1) * 4 + NP * 4 <= OP_STAGES * OP_BYTES, "centre-pick scratch");
   static_assert(M == 128 && KB % 32 == 0, "tile shape");
 };
 
@@ -166,12 +167,12 @@ __device__ __forceinline__ uint32_t sw128_offset(int row, int c16) {
 // 128-coordinate sample of the CTA's slice, score_i = sum of the
 // floor((n-1)/2) smallest sample distances D_ij.  Deterministic.  `scratch`
 // (>= 49 KB of shared memory) is the idle operand ring.
-template <int NT>
+template <int NT, int NP>
 __device__ int center_pick(const RowPtrs& rows, int n, int64_t d, int64_t k_begin, unsigned char* scratch) {
   constexpr int S = 128;                                   // sample coordinates
-  float* xs = reinterpret_cast<float*>(scratch);           // [n][S]
-  float* Ds = xs + GAR_MAX_N * S;                          // [64][65]
-  float* score = Ds + GAR_MAX_N * (GAR_MAX_N + 1);         // [64]
+  float* xs = reinterpret_cast<float*>(scratch);           // [NP][S]
+  float* Ds = xs + NP * S;                                 // [NP][NP+1]
+  float* score = Ds + NP * (NP + 1);                       // [NP]
   if (n <= 2) return 0;
   const int t = threadIdx.x;
   for (int e = t; e < n * (S / 4); e += NT) {
@@ -194,32 +195,32 @@ __device__ int center_pick(const RowPtrs& rows, int n, int64_t d, int64_t k_begi
       acc = fmaf(dx, dx, acc); acc = fmaf(dy, dy, acc); acc = fmaf(dz, dz, acc); acc = fmaf(dw, dw, acc);
     }
     if (!(acc <= 3.0e38f)) acc = __int_as_float(0x7f800000);
-    Ds[i * (GAR_MAX_N + 1) + j] = acc;
-    Ds[j * (GAR_MAX_N + 1) + i] = acc;
+    Ds[i * (NP + 1) + j] = acc;
+    Ds[j * (NP + 1) + i] = acc;
   }
   named_bar(3, NT);
   // score_i: sum (in j order) of the D_ij whose rank within row i (ties by j)
   // is below h -- the h smallest.  Ranks in parallel over (i, j) pairs.
   const int h = (n - 1) / 2;
-  float* kept = xs;                                        // [64][64] (sample no longer needed)
+  float* kept = xs;                                        // [NP][NP] (sample no longer needed)
   for (int e = t; e < n * n; e += NT) {
     const int i = e / n, j = e % n;
     float keep = 0.f;
     if (i != j) {
-      const float v = Ds[i * (GAR_MAX_N + 1) + j];
+      const float v = Ds[i * (NP + 1) + j];
       int rk = 0;
       for (int k = 0; k < n; ++k) {
-        const float w = Ds[i * (GAR_MAX_N + 1) + k];
+        const float w = Ds[i * (NP + 1) + k];
         rk += (k != i && (w < v || (w == v && k < j))) ? 1 : 0;
       }
       keep = (rk < h) ? v : 0.f;
     }
-    kept[i * GAR_MAX_N + j] = keep;
+    kept[i * NP + j] = keep;
   }
   named_bar(3, NT);
   if (t < n) {
     float sc = 0.f;
-    for (int j = 0; j < n; ++j) sc += kept[t * GAR_MAX_N + j];
+    for (int j = 0; j < n; ++j) sc += kept[t * NP + j];
     score[t] = sc;
   }
   named_bar(3, NT);
@@ -320,27 +321,31 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
     // producer's first raw stages are already in flight.  Per-coordinate
     // centring is a translation, so each CTA may pick its own row.
     constexpr int NT = C::CONV_WARPS * 32;
-    const int rc = center_pick<NT>(rows, n, d, t0 * C::KT, ops);
+    const int rc = center_pick<NT, NP>(rows, n, d, t0 * C::KT, ops);
     // zero the operand stages once: rows >= n are never written afterwards
     for (int q = threadIdx.x; q < C::OP_STAGES * C::OP_BYTES / 16; q += NT)
       reinterpret_cast<float4*>(ops)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     named_bar(3, NT);
     constexpr int RR = NP / 8;                  // rows per lane
+    constexpr int CH = C::CH;                   // float4 chunks per lane per tile
     const int g = lane & 7, cq = lane >> 3;
-    const int Q = 4 * warp + cq;                // float4 chunk index within the tile
-    // chunk Q -> block b, chunk qb within the block's K range
+    // per-lane chunks Q (float4 index within the tile) -> block b, chunk qb
     constexpr int QB = C::KB / 4;               // float4 chunks per block
-    const int b = Q / QB, qb = Q % QB;
-    // per-lane constant shared-memory offsets
-    const unsigned char* raw_me = raw + Q * 16 + g * C::RAW_PITCH;
-    const unsigned char* raw_c = raw + Q * 16 + rc * C::RAW_PITCH;
-    uint32_t off_hi[RR], off_lo[RR];
+    int Q[CH];
+    uint32_t off_hi[RR][CH], off_lo[RR][CH];
 #pragma unroll
-    for (int u = 0; u < RR; ++u) {
-      const int r = g + 8 * u;
-      off_hi[u] = (qb >> 3) * C::ATOM_BYTES + sw128_offset(b * NP + r, qb & 7);
-      off_lo[u] = (qb >> 3) * C::ATOM_BYTES + sw128_offset(C::N + b * NP + r, qb & 7);
+    for (int h = 0; h < CH; ++h) {
+      Q[h] = (4 * warp + cq) * CH + h;
+      const int b = Q[h] / QB, qb = Q[h] % QB;
+#pragma unroll
+      for (int u = 0; u < RR; ++u) {
+        const int r = g + 8 * u;
+        off_hi[u][h] = (qb >> 3) * C::ATOM_BYTES + sw128_offset(b * NP + r, qb & 7);
+        off_lo[u][h] = (qb >> 3) * C::ATOM_BYTES + sw128_offset(C::N + b * NP + r, qb & 7);
+      }
     }
+    const unsigned char* raw_me = raw + Q[0] * 16 + g * C::RAW_PITCH;   // chunks Q[0], Q[0]+1, ... are adjacent
+    const unsigned char* raw_c = raw + Q[0] * 16 + rc * C::RAW_PITCH;
     const int64_t R = (T + C::RAW_SUB - 1) / C::RAW_SUB;
     for (int64_t j = 0; j < R; ++j) {
       const int rs = static_cast<int>(j % C::RAW_STAGES);
@@ -357,36 +362,50 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
         // the tile holding coordinate d-1 may end in a (< 4-coordinate) chunk the
         // bulk copy skipped; only that tile pays for 64-bit bounds checks
         const bool last_tile = (t0 + i + 1) * C::KT > d;
-        float4 x[RR], c;
+        float4 x[RR][CH], c[CH];
         if (!last_tile) {
 #pragma unroll
-          for (int u = 0; u < RR; ++u)
-            if (g + 8 * u < n) x[u] = *reinterpret_cast<const float4*>(rt + u * 8 * C::RAW_PITCH);
-          c = *reinterpret_cast<const float4*>(rtc);
-        } else {
-          const int64_t k0 = (t0 + i) * C::KT + 4 * Q;
-          const bool ragged = k0 + 4 > d;
+          for (int h = 0; h < CH; ++h) {
 #pragma unroll
-          for (int u = 0; u < RR; ++u) {
-            const int r = g + 8 * u;
-            if (r < n) x[u] = ragged ? load_chunk(rows.p[r], k0, d) : *reinterpret_cast<const float4*>(rt + u * 8 * C::RAW_PITCH);
+            for (int u = 0; u < RR; ++u)
+              if (g + 8 * u < n) x[u][h] = *reinterpret_cast<const float4*>(rt + u * 8 * C::RAW_PITCH + h * 16);
+            c[h] = *reinterpret_cast<const float4*>(rtc + h * 16);
           }
-          c = ragged ? load_chunk(rows.p[rc], k0, d) : *reinterpret_cast<const float4*>(rtc);
+        } else {
+#pragma unroll
+          for (int h = 0; h < CH; ++h) {
+            const int64_t k0 = (t0 + i) * C::KT + 4 * Q[h];
+            const bool ragged = k0 + 4 > d;
+#pragma unroll
+            for (int u = 0; u < RR; ++u) {
+              const int r = g + 8 * u;
+              if (r < n)
+                x[u][h] = ragged ? load_chunk(rows.p[r], k0, d)
+                                 : *reinterpret_cast<const float4*>(rt + u * 8 * C::RAW_PITCH + h * 16);
+            }
+            c[h] = ragged ? load_chunk(rows.p[rc], k0, d) : *reinterpret_cast<const float4*>(rtc + h * 16);
+          }
         }
-        c = make_float4(fin(c.x), fin(c.y), fin(c.z), fin(c.w));   // centring c_k = fin(x_{r*,k})
+#pragma unroll
+        for (int h = 0; h < CH; ++h)    // centring c_k = fin(x_{r*,k})
+          c[h] = make_float4(fin(c[h].x), fin(c[h].y), fin(c[h].z), fin(c[h].w));
         if (i >= C::OP_STAGES) mbar_wait(&op_free[s], static_cast<uint32_t>(i / C::OP_STAGES - 1) & 1);
         unsigned char* At = ops + s * C::OP_BYTES;
 #pragma unroll
-        for (int u = 0; u < RR; ++u) {
-          if (g + 8 * u < n) {
-            float4 h, hi, lo;
-            h.x = __fsub_rn(x[u].x, c.x); h.y = __fsub_rn(x[u].y, c.y);
-            h.z = __fsub_rn(x[u].z, c.z); h.w = __fsub_rn(x[u].w, c.w);
-            hi.x = tf32_trunc(h.x); hi.y = tf32_trunc(h.y); hi.z = tf32_trunc(h.z); hi.w = tf32_trunc(h.w);
-            lo.x = __fsub_rn(h.x, hi.x); lo.y = __fsub_rn(h.y, hi.y);
-            lo.z = __fsub_rn(h.z, hi.z); lo.w = __fsub_rn(h.w, hi.w);
-            *reinterpret_cast<float4*>(At + off_hi[u]) = hi;
-            *reinterpret_cast<float4*>(At + off_lo[u]) = lo;
+        for (int h = 0; h < CH; ++h) {
+#pragma unroll
+          for (int u = 0; u < RR; ++u) {
+            if (g + 8 * u < n) {
+              const float4 xv = x[u][h], cv = c[h];
+              float4 hv, hi, lo;
+              hv.x = __fsub_rn(xv.x, cv.x); hv.y = __fsub_rn(xv.y, cv.y);
+              hv.z = __fsub_rn(xv.z, cv.z); hv.w = __fsub_rn(xv.w, cv.w);
+              hi.x = tf32_trunc(hv.x); hi.y = tf32_trunc(hv.y); hi.z = tf32_trunc(hv.z); hi.w = tf32_trunc(hv.w);
+              lo.x = __fsub_rn(hv.x, hi.x); lo.y = __fsub_rn(hv.y, hi.y);
+              lo.z = __fsub_rn(hv.z, hi.z); lo.w = __fsub_rn(hv.w, hi.w);
+              *reinterpret_cast<float4*>(At + off_hi[u][h]) = hi;
+              *reinterpret_cast<float4*>(At + off_lo[u][h]) = lo;
+            }
           }
         }
         fence_proxy_async_smem();
@@ -432,7 +451,10 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
     const int e = warp & 3;
     const int m = 32 * e + lane;
     const int blk = (m % C::N) / NP;
-    const int col0 = (C::BLOCKS > 1) ? blk * NP : (ew >> 2) * 32;
+    // useful columns of block blk: [blk*NP, blk*NP + NP); a 32-column load at
+    // col0 covers them starting at offset coff
+    const int col0 = (C::BLOCKS > 1) ? (blk * NP / 32) * 32 : (ew >> 2) * 32;
+    const int coff = (C::BLOCKS > 1) ? (blk * NP) % 32 : 0;
     double acc[C::EPI_COLS];
 #pragma unroll
     for (int j = 0; j < C::EPI_COLS; ++j) acc[j] = 0.0;
@@ -455,17 +477,21 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
     double* TB = reinterpret_cast<double*>(ops);          // [2NP][NP+1]; operand + raw rings are idle now
     const int tb_row = (m < C::N ? 0 : NP) + (m % NP);
     const int tb_col = (C::BLOCKS > 1) ? 0 : col0;
+    constexpr int USE = (C::BLOCKS > 1) ? NP : C::EPI_COLS;    // useful accumulator columns
     named_bar(2, EPI_THREADS);
-    if (blk == 0) {
 #pragma unroll
-      for (int j = 0; j < C::EPI_COLS; ++j) TB[tb_row * (NP + 1) + tb_col + j] = acc[j];
-    }
-    named_bar(2, EPI_THREADS);
-    if (blk == 1) {
+    for (int b = 0; b < C::BLOCKS; ++b) {       // fixed order: deterministic fp64 sums
+      if (blk == b) {
 #pragma unroll
-      for (int j = 0; j < C::EPI_COLS; ++j) TB[tb_row * (NP + 1) + tb_col + j] += acc[j];
+        for (int j = 0; j < C::EPI_COLS; ++j) {
+          if (j >= coff && j < coff + USE) {
+            double& dst = TB[tb_row * (NP + 1) + tb_col + j - coff];
+            dst = (b == 0) ? acc[j] : dst + acc[j];
+          }
+        }
+      }
+      named_bar(2, EPI_THREADS);
     }
-    named_bar(2, EPI_THREADS);
     double* P = partials + static_cast<size_t>(blockIdx.x) * n * n;
     for (int idx = threadIdx.x - C::EPI_WARP0 * 32; idx < n * n; idx += EPI_THREADS) {
       const int i = idx / n, j = idx % n;
@@ -502,6 +528,7 @@ cudaError_t launch_gram_partials(const float* const* rows, int n, int64_t d, dou
                                  int* n_parts, cudaStream_t stream) {
   RowPtrs rp;
   for (int i = 0; i < GAR_MAX_N; ++i) rp.p[i] = (i < n) ? rows[i] : nullptr;
+  if (n <= 16) return launch_np<16>(rp, n, d, partials, num_sms, n_parts, stream);
   if (n <= 32) return launch_np<32>(rp, n, d, partials, num_sms, n_parts, stream);
   return launch_np<64>(rp, n, d, partials, num_sms, n_parts, stream);
 }

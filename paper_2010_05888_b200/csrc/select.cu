@@ -86,8 +86,51 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const double* __res
     return;
   }
 
-  // Bulyan: theta rounds of Krum with removal (R7)
   const int theta = n - 2 * f;
+  if (n <= 32) {
+    // Bulyan, n <= 32: one warp, lane i holds row i's sorted distances in
+    // registers; each round sums the k smallest pool members in ascending
+    // order (the same fp64 additions as below) and a shuffle argmin picks the
+    // lowest (score, index).  No block barriers.
+    if (tid < 32) {
+      const int i = tid;
+      double row[31];
+      int rj[31];
+#pragma unroll
+      for (int e = 0; e < 31; ++e) {
+        const bool ok = i < n && e < n - 1;
+        row[e] = ok ? sd[i][e] : 0.0;
+        rj[e] = ok ? sj[i][e] : 63;
+      }
+      unsigned long long P = (1ull << n) - 1ull;
+      for (int t = 0; t < theta; ++t) {
+        const int k = max(__popcll(P) - f - 2, 0);
+        double sc = 0.0;
+        int taken = 0;
+#pragma unroll
+        for (int e = 0; e < 31; ++e) {
+          const bool take = ((P >> rj[e]) & 1ull) && taken < k;
+          if (take) sc += row[e];
+          taken += take ? 1 : 0;
+        }
+        double best = (i < n && ((P >> i) & 1ull)) ? sc : INFINITY;
+        int bi = (i < n && ((P >> i) & 1ull)) ? i : (1 << 30);
+        for (int off = 16; off > 0; off >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          if (key_lt(ob, oi, best, bi)) {
+            best = ob;
+            bi = oi;
+          }
+        }
+        if (i == 0) idx_out[t] = bi;
+        P &= ~(1ull << bi);
+      }
+    }
+    return;
+  }
+
+  // Bulyan: theta rounds of Krum with removal (R7)
   for (int t = 0; t < theta; ++t) {
     const unsigned long long P = pool;
     const int psize = __popcll(P);
