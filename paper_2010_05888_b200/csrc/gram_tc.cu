@@ -344,6 +344,9 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
         off_lo[u][h] = (qb >> 3) * C::ATOM_BYTES + sw128_offset(C::N + b * NP + r, qb & 7);
       }
     }
+    bool valid[RR];
+#pragma unroll
+    for (int u = 0; u < RR; ++u) valid[u] = g + 8 * u < n;
     const unsigned char* raw_me = raw + Q[0] * 16 + g * C::RAW_PITCH;   // chunks Q[0], Q[0]+1, ... are adjacent
     const unsigned char* raw_c = raw + Q[0] * 16 + rc * C::RAW_PITCH;
     const int64_t R = (T + C::RAW_SUB - 1) / C::RAW_SUB;
@@ -367,8 +370,8 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
 #pragma unroll
           for (int h = 0; h < CH; ++h) {
 #pragma unroll
-            for (int u = 0; u < RR; ++u)
-              if (g + 8 * u < n) x[u][h] = *reinterpret_cast<const float4*>(rt + u * 8 * C::RAW_PITCH + h * 16);
+            for (int u = 0; u < RR; ++u)   // rows >= n read stale ring data, never stored
+              x[u][h] = *reinterpret_cast<const float4*>(rt + u * 8 * C::RAW_PITCH + h * 16);
             c[h] = *reinterpret_cast<const float4*>(rtc + h * 16);
           }
         } else {
@@ -379,6 +382,7 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
 #pragma unroll
             for (int u = 0; u < RR; ++u) {
               const int r = g + 8 * u;
+              x[u][h] = make_float4(0.f, 0.f, 0.f, 0.f);
               if (r < n)
                 x[u][h] = ragged ? load_chunk(rows.p[r], k0, d)
                                  : *reinterpret_cast<const float4*>(rt + u * 8 * C::RAW_PITCH + h * 16);
@@ -389,22 +393,32 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
 #pragma unroll
         for (int h = 0; h < CH; ++h)    // centring c_k = fin(x_{r*,k})
           c[h] = make_float4(fin(c[h].x), fin(c[h].y), fin(c[h].z), fin(c[h].w));
+        // split every row unconditionally (rows >= n hold garbage and are simply
+        // not stored: their operand rows stay zero), so the compiler can
+        // interleave the independent rows instead of branching around each
+        float4 hiv[RR][CH], lov[RR][CH];
+#pragma unroll
+        for (int h = 0; h < CH; ++h) {
+#pragma unroll
+          for (int u = 0; u < RR; ++u) {
+            const float4 xv = x[u][h], cv = c[h];
+            float4 hv;
+            hv.x = __fsub_rn(xv.x, cv.x); hv.y = __fsub_rn(xv.y, cv.y);
+            hv.z = __fsub_rn(xv.z, cv.z); hv.w = __fsub_rn(xv.w, cv.w);
+            hiv[u][h] = make_float4(tf32_trunc(hv.x), tf32_trunc(hv.y), tf32_trunc(hv.z), tf32_trunc(hv.w));
+            lov[u][h] = make_float4(__fsub_rn(hv.x, hiv[u][h].x), __fsub_rn(hv.y, hiv[u][h].y),
+                                    __fsub_rn(hv.z, hiv[u][h].z), __fsub_rn(hv.w, hiv[u][h].w));
+          }
+        }
         if (i >= C::OP_STAGES) mbar_wait(&op_free[s], static_cast<uint32_t>(i / C::OP_STAGES - 1) & 1);
         unsigned char* At = ops + s * C::OP_BYTES;
 #pragma unroll
         for (int h = 0; h < CH; ++h) {
 #pragma unroll
           for (int u = 0; u < RR; ++u) {
-            if (g + 8 * u < n) {
-              const float4 xv = x[u][h], cv = c[h];
-              float4 hv, hi, lo;
-              hv.x = __fsub_rn(xv.x, cv.x); hv.y = __fsub_rn(xv.y, cv.y);
-              hv.z = __fsub_rn(xv.z, cv.z); hv.w = __fsub_rn(xv.w, cv.w);
-              hi.x = tf32_trunc(hv.x); hi.y = tf32_trunc(hv.y); hi.z = tf32_trunc(hv.z); hi.w = tf32_trunc(hv.w);
-              lo.x = __fsub_rn(hv.x, hi.x); lo.y = __fsub_rn(hv.y, hi.y);
-              lo.z = __fsub_rn(hv.z, hi.z); lo.w = __fsub_rn(hv.w, hi.w);
-              *reinterpret_cast<float4*>(At + off_hi[u][h]) = hi;
-              *reinterpret_cast<float4*>(At + off_lo[u][h]) = lo;
+            if (valid[u]) {
+              *reinterpret_cast<float4*>(At + off_hi[u][h]) = hiv[u][h];
+              *reinterpret_cast<float4*>(At + off_lo[u][h]) = lov[u][h];
             }
           }
         }
