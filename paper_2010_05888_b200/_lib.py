@@ -14,7 +14,9 @@ import re
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgar.so")
+# GAR_LIB_VARIANT: tools/ experiment builds (libgar_<variant>.so); never set by the product
+LIB_PATH = os.path.join(_HERE, "libgar.so" if not os.environ.get("GAR_LIB_VARIANT") else
+                        "libgar_" + os.environ["GAR_LIB_VARIANT"] + ".so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "gar.h")
 
 RULES = {"average": 0, "median": 1, "trimmed_mean": 2, "krum": 3, "multi_krum": 4, "bulyan": 5}
