@@ -66,31 +66,51 @@ __device__ __forceinline__ float avg_column(const float* col, int R, int stride)
   return static_cast<float>(s / R);
 }
 
+// The networks take values with NaN -> +inf only (fminf), not the full R1
+// canonicalisation: FMNMX orders -0 and +0 as equal, which can only swap
+// zeros; zeros add exactly nothing to an fp64 sum that starts at +0; and
+// Bulyan's closeness |y - med| and its value comparisons treat -0 == +0.
+// The median output is canonicalised, so every result equals that of the
+// canonical inputs.
+__device__ __forceinline__ float nan_to_inf(float v) { return fminf(v, __int_as_float(0x7f800000)); }
+
 template <int N>
 __device__ __forceinline__ float median_column(float* v) {
   gar_net::median_net<N>(v);
   if constexpr (N % 2 == 1) {
-    return v[(N - 1) / 2];
+    return __fadd_rn(v[(N - 1) / 2], 0.0f);
   } else {
-    return static_cast<float>((static_cast<double>(v[N / 2 - 1]) + static_cast<double>(v[N / 2])) * 0.5);
+    return static_cast<float>((static_cast<double>(__fadd_rn(v[N / 2 - 1], 0.0f)) +
+                               static_cast<double>(__fadd_rn(v[N / 2], 0.0f))) * 0.5);
+  }
+}
+
+// fp64 sum of v[F], ..., v[N-F-1] in ascending order (R2), F a compile-time
+// constant so only the kept values are converted and added.
+template <int N, int F>
+__device__ __forceinline__ double sum_kept(const float* v, int f) {
+  if constexpr (2 * F >= N) {
+    return 0.0;
+  } else {
+    if (f != F) return sum_kept<N, F + 1>(v, f);
+    double s = 0.0;
+#pragma unroll
+    for (int t = F; t < N - F; ++t) s += static_cast<double>(v[t]);
+    return s;
   }
 }
 
 template <int N>
 __device__ __forceinline__ float trimmed_column(float* v, int f) {
   gar_net::sort_net<N>(v);
-  double s = 0.0;
-#pragma unroll
-  for (int t = 0; t < N; ++t)
-    if (t >= f && t < N - f) s += static_cast<double>(v[t]);
-  return static_cast<float>(s / (N - 2 * f));
+  return static_cast<float>(sum_kept<N, 0>(v, f) / (N - 2 * f));
 }
 
 __device__ __forceinline__ float closeness(float y, float med) {
   return (y == med) ? 0.0f : fabsf(__fsub_rn(y, med));
 }
 
-// Bulyan coordinate phase over THETA canonical values (positions = ascending
+// Bulyan coordinate phase over THETA values (NaN -> +inf; zeros of either sign) (positions = ascending
 // input index).  Keeps the beta = THETA - 2f values with the smallest
 // (closeness, index) (R8) and averages them in ascending order (R2).
 //
@@ -236,7 +256,7 @@ __global__ void __launch_bounds__(32 * (W + kProducers), 1) coord_select_kernel(
       } else {
         float v[N > 0 ? N : 1];
 #pragma unroll
-        for (int r = 0; r < N; ++r) v[r] = canon(col[r * kTile]);
+        for (int r = 0; r < N; ++r) v[r] = nan_to_inf(col[r * kTile]);
         if constexpr (MODE == kModeMedian) {
           res = median_column<N>(v);
         } else if constexpr (MODE == kModeTrimmed) {
@@ -302,7 +322,7 @@ __global__ void __launch_bounds__(kLdgThreads) coord_ldg_kernel(const __grid_con
 #pragma unroll
       for (int r = 0; r < N; ++r) v[r] = __ldcs(rowp[r] + k);
 #pragma unroll
-      for (int r = 0; r < N; ++r) v[r] = canon(v[r]);
+      for (int r = 0; r < N; ++r) v[r] = nan_to_inf(v[r]);
       if constexpr (MODE == kModeMedian) {
         res = median_column<N>(v);
       } else if constexpr (MODE == kModeTrimmed) {

@@ -134,4 +134,6 @@ def adversarial_rows(n: int, d: int, seed: int) -> np.ndarray:
         x[:, 0] = np.float32(0.25)
         x[:, 1] = np.where(np.arange(n) % 2 == 0, np.float32(1.0), np.float32(-1.0))
         x[:, 2] = -0.0
+    if d >= 4:
+        x[:, 3] = np.where(np.arange(n) % 3 == 0, np.float32(0.0), np.float32(-0.0))   # mixed-sign zeros
     return x
