@@ -40,8 +40,15 @@ int coord_loader_ldg(int mode, int R) {
     return -1;
   }();
   if (forced >= 0) return forced;
-  if (mode != kModeBulyan && R <= 32) return 0;
-  return 1;
+  // Measured per mode on B200 across n = 7..63 (profiles/r1_loader_choice.md):
+  // the TMA ring wins for Median up to 32 rows, for averages above 16 rows and
+  // for the trimmed mean at 29..32 rows; direct loads win elsewhere.
+  switch (mode) {
+    case kModeMedian: return R <= 32 ? 0 : 1;
+    case kModeAverage: return (R > 16 && R <= 32) ? 0 : 1;
+    case kModeTrimmed: return (R > 28 && R <= 32) ? 0 : 1;
+    default: return 1;
+  }
 }
 
 inline cudaError_t launch_copy_row(const CoordLaunch& L, cudaStream_t stream) {
