@@ -2,12 +2,13 @@
 """Generate ``networks.cuh``: straight-line compare-exchange networks for the
 coordinate-selection kernel (product code; shares nothing with oracle/).
 
-For every size N in 1..64 we take Batcher's odd-even merge sort (and the
-bitonic sort) on the next power of two P >= N, with wires N..P-1 holding the
-constant +inf, constant-propagate the padding (a comparator against a +inf
-wire is a no-op or a relabel), then keep only the min/max outputs that reach
-the requested output positions.  The cheaper of the two constructions (in
-emitted min/max instructions) is kept per (N, outputs).
+For every size N in 1..64 we take four constructions: Batcher's odd-even
+merge sort, the bitonic sort and Parberry's pairwise network on the next power
+of two P >= N (wires N..P-1 hold the constant +inf, and the padding is
+constant-propagated: a comparator against a +inf wire is a no-op or a
+relabel), and Batcher's merge exchange on exactly N wires.  Only the min/max
+outputs that reach the requested output positions are kept, and the cheapest
+construction (in emitted min/max instructions) wins per (N, outputs).
 
 Emitted functions (all in-place on ``float v[N]``, ascending order):
 
@@ -68,6 +69,58 @@ def bitonic_sort(P):
     return comps
 
 
+def merge_exchange(N):
+    """Batcher's merge exchange for any N (Knuth, TAOCP 5.2.2, Algorithm M):
+    no padding wires."""
+    comps = []
+    t = 1
+    while (1 << t) < N:
+        t += 1
+    p = 1 << (t - 1)
+    while p > 0:
+        q, r, dd = 1 << (t - 1), 0, p
+        while True:
+            for i in range(N - dd):
+                if (i & p) == r:
+                    comps.append((i, i + dd))
+            if q == p:
+                break
+            dd, q, r = q - p, q >> 1, p
+        p >>= 1
+    return comps
+
+
+def pairwise_sort(P):
+    """Parberry's pairwise sorting network for P = 2^k wires."""
+    comps = []
+    a = 1
+    while a < P:
+        b, c = a, 0
+        while b < P:
+            comps.append((b - a, b))
+            b += 1
+            c = (c + 1) % a
+            if c == 0:
+                b += a
+        a *= 2
+    a //= 4
+    e = 1
+    while a > 0:
+        d = e
+        while d > 0:
+            b, c = (d + 1) * a, 0
+            while b < P:
+                comps.append((b - d * a, b))
+                b += 1
+                c = (c + 1) % a
+                if c == 0:
+                    b += a
+            d //= 2
+        a //= 2
+        e = e * 2 + 1
+    return comps
+
+
 def build_ssa(N, comps):
     """Symbolic execution.  Wire contents are ('in', i), ('inf',) or ('op', id).
     Returns (ops, final) where ops[id] = (kind, a, b) with kind in {min,max}."""
@@ -113,7 +166,8 @@ def best_network(N, positions):
     while P < N:
         P *= 2
     best = None
-    for name, comps in (("oddeven", oddeven_merge_sort(P)), ("bitonic", bitonic_sort(P))):
+    for name, comps in (("oddeven", oddeven_merge_sort(P)), ("bitonic", bitonic_sort(P)),
+                        ("merge-exchange", merge_exchange(N)), ("pairwise", pairwise_sort(P))):
         ops, final = build_ssa(N, comps)
         live = live_ops(ops, [final[p] for p in positions])
         cost = len(live)
