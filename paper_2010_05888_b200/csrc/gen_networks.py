@@ -13,7 +13,9 @@ construction (in emitted min/max instructions) wins per (N, outputs).
 Emitted functions (all in-place on ``float v[N]``, ascending order):
 
 * ``gar_net::sort_<N>(v)``    — full sort, every position valid;
-* ``gar_net::median_<N>(v)``  — only v[(N-1)/2] (and v[N/2] for even N) valid.
+* ``gar_net::median_<N>(v)``  — only v[(N-1)/2] (and v[N/2] for even N) valid;
+* ``gar_net::trim_<N>(v)``    — v[F..N-F-1] valid and sorted, F = trim_f<N>() =
+  max(0, (N-3)/4): the trimmed mean at the paper's f for n = 4f+3.
 
 Values must be canonical (no NaN, no -0): the kernel canonicalises first, so
 fminf/fmaxf (FMNMX) implement an exact compare-exchange.
@@ -204,7 +206,9 @@ def verify(N, ops, final, positions, trials=2000):
 def emit(N, fname, positions):
     cost, name, ops, final, live = best_network(N, positions)
     verify(N, ops, final, positions, trials=600 if N > 12 else (1 << N))
-    lines = [f"// N={N}: {name}, {cost} min/max ({'full sort' if len(positions) == N else 'median'})",
+    what = "full sort" if len(positions) == N else ("median" if len(positions) <= 2 else
+                                                       f"positions {positions[0]}..{positions[-1]}")
+    lines = [f"// N={N}: {name}, {cost} min/max ({what})",
              f"__device__ __forceinline__ void {fname}_{N}(float* v) {{"]
     names = {}
 
@@ -228,6 +232,10 @@ def emit(N, fname, positions):
     return "\n".join(lines), cost
 
 
+def trim_f(N):
+    return (N - 3) // 4 if N >= 3 else 0
+
+
 def main(out_path):
     parts = ["// GENERATED by gen_networks.py — do not edit.  Product code (libgar);",
              "// shares nothing with oracle/.  Pruned Batcher / bitonic networks with",
@@ -240,15 +248,21 @@ def main(out_path):
         med = [(N - 1) // 2] if N % 2 else [N // 2 - 1, N // 2]
         src, c_med = emit(N, "median", med)
         parts.append(src)
-        table.append((N, c_sort, c_med))
+        F = trim_f(N)
+        src, c_trim = emit(N, "trim", list(range(F, N - F)))
+        parts.append(src)
+        table.append((N, c_sort, c_med, c_trim))
     parts.append("template <int N> __device__ __forceinline__ void sort_net(float* v);")
+    parts.append("template <int N> __device__ __forceinline__ void trim_net(float* v);")
+    parts.append("template <int N> constexpr int trim_f() { return N >= 3 ? (N - 3) / 4 : 0; }")
     parts.append("template <int N> __device__ __forceinline__ void median_net(float* v);")
     for N in range(1, MAXN + 1):
         parts.append(f"template <> __device__ __forceinline__ void sort_net<{N}>(float* v) {{ sort_{N}(v); }}")
         parts.append(f"template <> __device__ __forceinline__ void median_net<{N}>(float* v) {{ median_{N}(v); }}")
-    parts.append("// min/max instruction counts (N, sort, median):")
-    for N, a, b in table:
-        parts.append(f"//   {N:2d} {a:4d} {b:4d}")
+        parts.append(f"template <> __device__ __forceinline__ void trim_net<{N}>(float* v) {{ trim_{N}(v); }}")
+    parts.append("// min/max instruction counts (N, sort, median, trim at F = trim_f<N>):")
+    for N, a, b, c in table:
+        parts.append(f"//   {N:2d} {a:4d} {b:4d} {c:4d}")
     parts.append("}  // namespace gar_net")
     with open(out_path, "w") as fh:
         fh.write("\n".join(parts) + "\n")

@@ -72,7 +72,9 @@ def test_every_n_coordinatewise(gar, n):
     x[:, :50] = rng.integers(-2, 3, (n, 50)).astype(np.float32)      # ties
     f = (n - 1) // 2
     check_rule(gar, "median", x, f)
-    check_rule(gar, "trimmed_mean", x, f // 2)
+    # the paper's f (n = 4f + 3, a pruned network) and other trims (full sort)
+    for ft in sorted({0, f // 2, max(0, (n - 3) // 4), f}):
+        check_rule(gar, "trimmed_mean", x, ft)
     check_rule(gar, "average", x, 0)
 
 
