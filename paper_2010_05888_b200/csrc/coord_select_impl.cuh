@@ -180,6 +180,65 @@ __device__ __forceinline__ float bulyan_column(float* v, float* col, int stride,
   return static_cast<float>(acc / beta);
 }
 
+// Bulyan coordinate phase when beta = 3, i.e. f = (THETA-3)/2 (n = 4f + 3,
+// P:556; every BASELINE configuration), THETA odd >= 5.  The kept window
+// starts at h-2, h-1 or h (it holds the median itself, closeness 0), so a
+// network that sorts only positions h-2..h+2 suffices and the window stays in
+// registers.  A closeness tie between two different values takes the exact
+// definition: the beta values of smallest (closeness, index) over the
+// index-ordered canonical inputs, summed in ascending order.
+template <int THETA>
+__device__ __forceinline__ float bulyan_column_b3(float* v, const float* const* rowp, int64_t gidx) {
+  static_assert(THETA % 2 == 1 && THETA >= 5, "beta = 3 window");
+  constexpr int h = (THETA - 1) / 2;
+  gar_net::window_net<THETA>(v);
+  const float a0 = v[h - 2], a1 = v[h - 1], med = v[h], a3 = v[h + 1], a4 = v[h + 2];
+  const float c0 = closeness(a0, med), c1 = closeness(a1, med);
+  const float c3 = closeness(a3, med), c4 = closeness(a4, med);
+  const int shift = ((c3 < c0) ? 1 : 0) + ((c4 < c1) ? 1 : 0);
+  const bool tie = (c3 == c0 && a3 != a0) || (c4 == c1 && a4 != a1);
+  float k0, k1, k2;
+  if (!tie) {
+    k0 = shift == 0 ? a0 : (shift == 1 ? a1 : med);
+    k1 = shift == 0 ? a1 : (shift == 1 ? med : a3);
+    k2 = shift == 0 ? med : (shift == 1 ? a3 : a4);
+  } else {
+    float kept[3] = {0.f, 0.f, 0.f};
+    int nk = 0;
+    for (int t = 0; t < THETA; ++t) {
+      const float yt = canon(__ldg(rowp[t] + gidx));
+      const float ct = closeness(yt, med);
+      int rank = 0;
+      for (int u = 0; u < THETA; ++u) {
+        const float cu = closeness(canon(__ldg(rowp[u] + gidx)), med);
+        rank += (cu < ct || (cu == ct && u < t)) ? 1 : 0;
+      }
+      if (rank < 3 && nk < 3) kept[nk++] = yt;
+    }
+    k0 = fminf(kept[0], kept[1]);
+    k1 = fmaxf(kept[0], kept[1]);
+    k2 = fmaxf(k1, kept[2]);
+    k1 = fminf(k1, kept[2]);
+    const float lo = fminf(k0, k1);
+    k1 = fmaxf(k0, k1);
+    k0 = lo;
+  }
+  double acc = 0.0;
+  acc += static_cast<double>(k0);
+  acc += static_cast<double>(k1);
+  acc += static_cast<double>(k2);
+  return static_cast<float>(acc / 3);
+}
+
+template <int THETA>
+__device__ __forceinline__ float bulyan_dispatch(float* v, float* col, int stride, int f,
+                                                 const float* const* rowp, int64_t gidx) {
+  if constexpr (THETA % 2 == 1 && THETA >= 5) {
+    if (f == (THETA - 3) / 2) return bulyan_column_b3<THETA>(v, rowp, gidx);
+  }
+  return bulyan_column<THETA>(v, col, stride, f, rowp, gidx);
+}
+
 // ---------------------------------------------------------------- the kernel
 template <int MODE, int N, int W>
 __global__ void __launch_bounds__(32 * (W + kProducers), 1) coord_select_kernel(const __grid_constant__ CoordParams p) {
@@ -273,7 +332,7 @@ __global__ void __launch_bounds__(32 * (W + kProducers), 1) coord_select_kernel(
         } else if constexpr (MODE == kModeTrimmed) {
           res = trimmed_column<N>(v, p.f);
         } else {
-          res = bulyan_column<N>(v, col, kTile, p.f, rowp, start + c);
+          res = bulyan_dispatch<N>(v, col, kTile, p.f, rowp, start + c);
         }
       }
       store_result(p.out, p.extra, start + c, res);
@@ -340,7 +399,7 @@ __global__ void __launch_bounds__(kLdgThreads) coord_ldg_kernel(const __grid_con
         res = trimmed_column<N>(v, p.f);
       } else {
         float* col = reinterpret_cast<float*>(ldg_smem) + threadIdx.x;
-        res = bulyan_column<N>(v, col, kLdgThreads, p.f, rowp, k);
+        res = bulyan_dispatch<N>(v, col, kLdgThreads, p.f, rowp, k);
       }
     }
     store_result(p.out, p.extra, k, res);

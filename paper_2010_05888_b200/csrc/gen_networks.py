@@ -15,7 +15,9 @@ Emitted functions (all in-place on ``float v[N]``, ascending order):
 * ``gar_net::sort_<N>(v)``    — full sort, every position valid;
 * ``gar_net::median_<N>(v)``  — only v[(N-1)/2] (and v[N/2] for even N) valid;
 * ``gar_net::trim_<N>(v)``    — v[F..N-F-1] valid and sorted, F = trim_f<N>() =
-  max(0, (N-3)/4): the trimmed mean at the paper's f for n = 4f+3.
+  max(0, (N-3)/4): the trimmed mean at the paper's f for n = 4f+3 (P:556);
+* ``gar_net::window_<N>(v)``  — odd N >= 5: v[h-2..h+2] valid and sorted,
+  h = (N-1)/2: Bulyan's coordinate phase when beta = 3 (n = 4f+3).
 
 Values must be canonical (no NaN, no -0): the kernel canonicalises first, so
 fminf/fmaxf (FMNMX) implement an exact compare-exchange.
@@ -208,6 +210,8 @@ def emit(N, fname, positions):
     verify(N, ops, final, positions, trials=600 if N > 12 else (1 << N))
     what = "full sort" if len(positions) == N else ("median" if len(positions) <= 2 else
                                                        f"positions {positions[0]}..{positions[-1]}")
+    if len(positions) == N and N <= 2:
+        what = "full sort"
     lines = [f"// N={N}: {name}, {cost} min/max ({what})",
              f"__device__ __forceinline__ void {fname}_{N}(float* v) {{"]
     names = {}
@@ -251,15 +255,22 @@ def main(out_path):
         F = trim_f(N)
         src, c_trim = emit(N, "trim", list(range(F, N - F)))
         parts.append(src)
+        if N % 2 == 1 and N >= 5:
+            h = (N - 1) // 2
+            src, _ = emit(N, "window", list(range(h - 2, h + 3)))
+            parts.append(src)
         table.append((N, c_sort, c_med, c_trim))
     parts.append("template <int N> __device__ __forceinline__ void sort_net(float* v);")
     parts.append("template <int N> __device__ __forceinline__ void trim_net(float* v);")
+    parts.append("template <int N> __device__ __forceinline__ void window_net(float* v);")
     parts.append("template <int N> constexpr int trim_f() { return N >= 3 ? (N - 3) / 4 : 0; }")
     parts.append("template <int N> __device__ __forceinline__ void median_net(float* v);")
     for N in range(1, MAXN + 1):
         parts.append(f"template <> __device__ __forceinline__ void sort_net<{N}>(float* v) {{ sort_{N}(v); }}")
         parts.append(f"template <> __device__ __forceinline__ void median_net<{N}>(float* v) {{ median_{N}(v); }}")
         parts.append(f"template <> __device__ __forceinline__ void trim_net<{N}>(float* v) {{ trim_{N}(v); }}")
+        if N % 2 == 1 and N >= 5:
+            parts.append(f"template <> __device__ __forceinline__ void window_net<{N}>(float* v) {{ window_{N}(v); }}")
     parts.append("// min/max instruction counts (N, sort, median, trim at F = trim_f<N>):")
     for N, a, b, c in table:
         parts.append(f"//   {N:2d} {a:4d} {b:4d} {c:4d}")

@@ -90,7 +90,8 @@ def test_every_family_size(gar, n):
         check_rule(gar, "multi_krum", x, f_k, m=1)
 
 
-@pytest.mark.parametrize("theta,f", [(3, 0), (5, 1), (7, 1), (9, 2), (12, 3), (17, 7), (33, 15), (64, 0)])
+@pytest.mark.parametrize("theta,f", [(3, 0), (5, 1), (7, 1), (7, 2), (9, 2), (9, 3), (11, 4), (12, 3), (17, 7),
+                                     (19, 8), (33, 15), (64, 0)])
 def test_bulyan_coordinate_phase_ties(gar, theta, f):
     """Integer-valued rows force closeness ties between different values
     (exercises the exact rank-count path); the selection is given explicitly
