@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--workload", default="C3", help="C1..C4 or sweep:<n>")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--output", default="fused", choices=["replicated", "sharded", "fused"],
+    ap.add_argument("--output", default="fused",
+                    choices=["replicated", "replicated-async", "sharded", "fused", "fused-mc"],
                     help="N>1: all-gather the aggregate to every rank with NCCL (north_star), write it into every "
                          "rank's buffer from the producing kernel over NVLink (fused), or keep it d-sharded")
     return ap.parse_args()
@@ -190,6 +191,8 @@ def run_ours(args):
                 segs.append((CLASS[label], r, last[0], e))
                 last[0] = e
             aggs[r].aggregate(X, out_local=outs[r], out_full=full[r], mark=mark)
+        for r in RULES:              # output="replicated-async": the step ends when every gather has
+            aggs[r].wait()           # landed (they overlap the following rules' kernels)
 
     for _ in range(args.warmup):
         step(False)
@@ -255,6 +258,7 @@ def run_ours(args):
                 if r in rule_drained:              # fused outputs live in the aggregator's own buffer
                     stream.wait_event(rule_drained[r])
                 res = aggs[r].aggregate(xbuf[bb], out_local=obuf[bb][r], out_full=fbuf[bb][r])
+                aggs[r].wait()
                 local_res = res[lo:hi] if res.numel() > dl else res
                 done = torch.cuda.Event()
                 done.record(stream)
@@ -319,7 +323,8 @@ def run_ours(args):
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: n={n} f={f} d={d}, GARs {'/'.join(RULES)}",
                    "n": n, "f": f, "d": d, "parallelism": f"d-sharded x{world}" if world > 1 else "single GPU",
-                   "output": args.output if world > 1 else "local",
+                   "output": (args.output + (f" ({aggs[RULES[0]].fused_path})" if aggs[RULES[0]].fused_path else ""))
+                   if world > 1 else "local",
                    "l2": f"inputs {n * d * 4 / 1e9:.2f} GB > 126 MB L2 (no flush needed)"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": kernels[dom]["frac"],

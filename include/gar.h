@@ -157,6 +157,25 @@ gar_status gar_combine_bcast(gar_rule rule, const float* const* grads, int n, in
                              int64_t d_local, const int32_t* indices_dev, float* out,
                              float* const* extra_outs, int n_extra, gar_stream_t stream);
 
+/* gar_aggregate_mcast / gar_combine_mcast: gar_aggregate_ex / gar_combine
+ * with the result written through a MULTICAST address instead (the d-sharded
+ * output all-gather the north_star names, done by the
+ * producing kernel over NVLink SHARP): out_mc is the multicast virtual
+ * address (e.g. torch symmetric memory's multicast_ptr + byte offset) of the
+ * region whose local mapping is `out`; each result is stored once with
+ * multimem.st and the NVSwitch writes it into every member GPU's buffer,
+ * `out` included, so nothing is stored to `out` directly.  out_mc: non-null,
+ * 16-byte aligned (GAR_ERR_INVALID_ARGUMENT / GAR_ERR_ALIGNMENT), not checked
+ * with cudaPointerGetAttributes.  Visibility on the other GPUs needs the
+ * caller's cross-GPU barrier after the call, as for the _bcast variants. */
+gar_status gar_aggregate_mcast(gar_rule rule, const float* const* grads, int n, int f, int m,
+                               int64_t d, float* out, float* out_mc, int32_t* indices_dev,
+                               void* workspace, size_t workspace_bytes, gar_stream_t stream);
+
+gar_status gar_combine_mcast(gar_rule rule, const float* const* grads, int n, int f, int m,
+                             int64_t d_local, const int32_t* indices_dev, float* out, float* out_mc,
+                             gar_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

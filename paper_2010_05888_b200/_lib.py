@@ -54,6 +54,8 @@ def _load():
         "gar_combine": ([I, PP, I, I, I, I64, P, P, P], I),
         "gar_aggregate_bcast": ([I, PP, I, I, I, I64, P, PP, I, P, P, SZ, P], I),
         "gar_combine_bcast": ([I, PP, I, I, I, I64, P, P, PP, I, P], I),
+        "gar_aggregate_mcast": ([I, PP, I, I, I, I64, P, P, P, P, SZ, P], I),
+        "gar_combine_mcast": ([I, PP, I, I, I, I64, P, P, P, P], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -246,4 +248,23 @@ def gar_combine_bcast(rule, grads, f: int, m: int, indices: torch.Tensor, out: t
     ex, ne = _ptr_array(extra_ptrs)
     check(lib.gar_combine_bcast(rule_id(rule), arr, n, f, m, d, _ptr(indices), _ptr(out), ex, ne,
                                 stream_handle(dev, stream)), "gar_combine_bcast")
+    return out
+
+
+def gar_aggregate_mcast(rule, grads, f: int, m: int, out: torch.Tensor, out_mc: int, indices=None, workspace=None,
+                        d: int | None = None, stream=None):
+    """gar_aggregate_ex with the result stored through the multicast address
+    out_mc (an int) that maps `out` on every member GPU."""
+    arr, n, d, dev = row_pointers(grads, d)
+    wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    check(lib.gar_aggregate_mcast(rule_id(rule), arr, n, f, m, d, _ptr(out), ctypes.c_void_p(out_mc), _ptr(indices),
+                                  _ptr(workspace), wsb, stream_handle(dev, stream)), "gar_aggregate_mcast")
+    return out
+
+
+def gar_combine_mcast(rule, grads, f: int, m: int, indices: torch.Tensor, out: torch.Tensor, out_mc: int,
+                      d: int | None = None, stream=None):
+    arr, n, d, dev = row_pointers(grads, d)
+    check(lib.gar_combine_mcast(rule_id(rule), arr, n, f, m, d, _ptr(indices), _ptr(out), ctypes.c_void_p(out_mc),
+                                stream_handle(dev, stream)), "gar_combine_mcast")
     return out

@@ -19,13 +19,33 @@ struct RowPtrs {
 // GPUs' replicated output buffers, mapped into this GPU's address space
 // (symmetric memory), so the stores travel over NVLink inside the producing
 // kernel instead of in a separate all-gather.
+//
+// Or, with mc set, a multicast address (NVLink SHARP / NVLS):
+// one multimem.st per result is replicated by the NVSwitch into every GPU's
+// buffer, this GPU's included, so each GPU sends its slice over NVLink once
+// instead of once per peer; the local and peer stores are skipped.
 #define GAR_MAX_PEERS 8
 struct OutPtrs {
   float* p[GAR_MAX_PEERS];
   int n;
+  float* mc;
 };
 
+__device__ __forceinline__ void mc_store(float* addr, float v) {
+  asm volatile("multimem.st.global.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
+}
+
+__device__ __forceinline__ void mc_store4(float* addr, float4 v) {
+  asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
 __device__ __forceinline__ void store_result(float* out, const OutPtrs& extra, int64_t i, float v) {
+  if (extra.mc) {
+    mc_store(extra.mc + i, v);
+    return;
+  }
   __stcs(out + i, v);
   for (int j = 0; j < extra.n; ++j) extra.p[j][i] = v;
 }

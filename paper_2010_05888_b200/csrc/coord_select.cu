@@ -17,6 +17,10 @@ __global__ void __launch_bounds__(256) copy_row_kernel(const __grid_constant__ R
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n4; q += int64_t(gridDim.x) * blockDim.x) {
     float4 v = __ldcs(reinterpret_cast<const float4*>(src) + q);
     v.x = __fadd_rn(v.x, 0.0f); v.y = __fadd_rn(v.y, 0.0f); v.z = __fadd_rn(v.z, 0.0f); v.w = __fadd_rn(v.w, 0.0f);
+    if (extra.mc) {
+      mc_store4(extra.mc + 4 * q, v);
+      continue;
+    }
     __stcs(reinterpret_cast<float4*>(out) + q, v);
     for (int j = 0; j < extra.n; ++j) reinterpret_cast<float4*>(extra.p[j])[q] = v;
   }

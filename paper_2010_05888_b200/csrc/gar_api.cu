@@ -216,6 +216,16 @@ gar_status make_extra(float* const* extra_outs, int n_extra, gar::OutPtrs* extra
   return GAR_OK;
 }
 
+// Multicast destination (NVLS): non-null, 16-byte aligned; a multicast
+// virtual address is not checked with cudaPointerGetAttributes.
+gar_status make_mc(float* out_mc, gar::OutPtrs* extra) {
+  *extra = gar::OutPtrs{};
+  if (!out_mc) return GAR_ERR_INVALID_ARGUMENT;
+  if (reinterpret_cast<uintptr_t>(out_mc) & 15u) return GAR_ERR_ALIGNMENT;
+  extra->mc = out_mc;
+  return GAR_OK;
+}
+
 gar_status aggregate_impl(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d, float* out,
                           const gar::OutPtrs& extra, int32_t* indices_dev, void* workspace, size_t workspace_bytes,
                           gar_stream_t stream) {
@@ -410,6 +420,23 @@ gar_status gar_combine_bcast(gar_rule rule, const float* const* grads, int n, in
                              gar_stream_t stream) {
   gar::OutPtrs extra{};
   gar_status s = make_extra(extra_outs, n_extra, &extra);
+  if (s != GAR_OK) return s;
+  return combine_impl(rule, grads, n, f, m, d_local, indices_dev, out, extra, stream);
+}
+
+gar_status gar_aggregate_mcast(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d,
+                               float* out, float* out_mc, int32_t* indices_dev, void* workspace,
+                               size_t workspace_bytes, gar_stream_t stream) {
+  gar::OutPtrs extra{};
+  gar_status s = make_mc(out_mc, &extra);
+  if (s != GAR_OK) return s;
+  return aggregate_impl(rule, grads, n, f, m, d, out, extra, indices_dev, workspace, workspace_bytes, stream);
+}
+
+gar_status gar_combine_mcast(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d_local,
+                             const int32_t* indices_dev, float* out, float* out_mc, gar_stream_t stream) {
+  gar::OutPtrs extra{};
+  gar_status s = make_mc(out_mc, &extra);
   if (s != GAR_OK) return s;
   return combine_impl(rule, grads, n, f, m, d_local, indices_dev, out, extra, stream);
 }

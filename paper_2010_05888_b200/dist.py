@@ -17,8 +17,12 @@ coordinates).  Then:
 * the aggregate is all-gathered (``output="replicated"``: NCCL all-gather
   after the kernel, the north_star default), written by the producing kernel
   itself into every GPU's output buffer over NVLink (``output="fused"``:
-  torch symmetric memory, ``gar_*_bcast``; one device-side barrier), or left
-  d-sharded (``output="sharded"``, what a ZeRO-style optimizer consumes).
+  torch symmetric memory, one store per peer, ``gar_*_bcast``; or with
+  ``"fused-mc"`` one NVLink SHARP multicast store per result, ``gar_*_mcast``;
+  then one device-side barrier), all-gathered by NCCL asynchronously so the
+  transfer overlaps the caller's next work (``"replicated-async"``, then
+  ``wait()``), or left d-sharded (``output="sharded"``, what a ZeRO-style
+  optimizer consumes).
 
 The paper's own exchange is PyTorch ``broadcast``/``gather`` over NCCL or gloo
 (§4.2); here the only collectives are one tiny
@@ -66,13 +70,29 @@ class _LibgarBackend:
         return self._lib.gar_select_from_gram(rule, gram, n, f, m, idx)
 
     def combine(self, rule, rows, f, m, idx, out, d, extra=()):
-        if extra:
+        if isinstance(extra, Multicast):
+            self._lib.gar_combine_mcast(rule, rows, f, m, idx, out, extra.addr, d=d)
+        elif extra:
             self._lib.gar_combine_bcast(rule, rows, f, m, idx, out, extra, d=d)
         else:
             self._lib.gar_combine(rule, rows, f, m, idx, out, d=d)
 
     def coordinatewise_bcast(self, agg, rows, out, d, extra):
-        self._lib.gar_aggregate_bcast(agg.rule, rows, agg.f, agg.m, out, extra, workspace=None, d=d)
+        if isinstance(extra, Multicast):
+            self._lib.gar_aggregate_mcast(agg.rule, rows, agg.f, agg.m, out, extra.addr, workspace=None, d=d)
+        else:
+            self._lib.gar_aggregate_bcast(agg.rule, rows, agg.f, agg.m, out, extra, workspace=None, d=d)
+
+
+class Multicast:
+    """Fused-output destination given as one multicast (NVLS) address: the
+    kernel's multimem stores reach every rank's buffer, this rank's included."""
+
+    def __init__(self, addr: int):
+        self.addr = int(addr)
+
+    def __bool__(self):
+        return True
 
 
 class ShardedAggregator:
@@ -81,7 +101,7 @@ class ShardedAggregator:
 
     def __init__(self, rule: str, n: int, f: int, d: int, m: int | None = None, group=None,
                  output: str = "replicated", backend=None):
-        if output not in ("replicated", "sharded", "fused"):
+        if output not in ("replicated", "replicated-async", "sharded", "fused", "fused-mc"):
             raise ValueError(output)
         self.rule, self.n, self.f, self.d = rule, int(n), int(f), int(d)
         self.m = 0 if m is None else int(m)
@@ -98,19 +118,34 @@ class ShardedAggregator:
         self._gram = None
         self._idx = None
         self._pad = None
-        self._symm = None          # (symmetric out_full, handle, extra peer addresses) for output="fused"
+        self._symm = None          # (symmetric out_full, handle, Multicast | peer addresses) for fused output
 
     def _fused_buffers(self, device):
-        """Replicated output in symmetric memory; the addresses of this rank's
-        slice in every OTHER rank's buffer (peer-mapped over NVLink)."""
+        """Replicated output in symmetric memory, and where the kernel stores
+        this rank's slice: the slice's addresses in every OTHER rank's buffer
+        (peer-mapped over NVLink, one store per peer), or with
+        output="fused-mc" and a multicast-capable group the multicast address
+        of the slice (NVLS: one store per result, replicated by the NVSwitch;
+        measured slower than the peer stores on B200, profiles/)."""
         if self._symm is None:
             import torch.distributed._symmetric_memory as symm_mem
             buf = symm_mem.empty(self.per * self.world, dtype=torch.float32, device=device)
             group = self.group if self.group is not None else dist.group.WORLD
             handle = symm_mem.rendezvous(buf, group)
-            extra = [int(handle.buffer_ptrs[r]) + 4 * self.lo for r in range(self.world) if r != self.rank]
+            mc = int(handle.multicast_ptr or 0)
+            if mc and self.output == "fused-mc":
+                extra = Multicast(mc + 4 * self.lo)
+            else:
+                extra = [int(handle.buffer_ptrs[r]) + 4 * self.lo for r in range(self.world) if r != self.rank]
             self._symm = (buf, handle, extra)
         return self._symm
+
+    @property
+    def fused_path(self) -> str | None:
+        """"multicast" / "p2p" once the fused buffers exist, else None."""
+        if self._symm is None:
+            return None
+        return "multicast" if isinstance(self._symm[2], Multicast) else "p2p"
 
     # -- lazily created per-device state ------------------------------------------
     def _state(self, device):
@@ -136,7 +171,7 @@ class ShardedAggregator:
         dev = rows_local.device if isinstance(rows_local, torch.Tensor) else rows_local[0].device
         self._state(dev)
         mark = mark or (lambda label: None)
-        if self.output == "fused" and self.world > 1:
+        if self.output in ("fused", "fused-mc") and self.world > 1:
             return self._aggregate_fused(rows_local, dev, mark)
         if out_local is None:
             out_local = torch.empty(self.d_local, dtype=torch.float32, device=dev)
@@ -157,15 +192,26 @@ class ShardedAggregator:
             return out_local
         if out_full is None:
             out_full = torch.empty(self.per * self.world, dtype=torch.float32, device=dev)
-        if self.d_local == self.per:
-            dist.all_gather_into_tensor(out_full, out_local, group=self.group)
-        else:
+        src = out_local
+        if self.d_local != self.per:
             if self._pad is None:
                 self._pad = torch.zeros(self.per, dtype=torch.float32, device=dev)
             self._pad[: self.d_local].copy_(out_local)
-            dist.all_gather_into_tensor(out_full, self._pad, group=self.group)
+            src = self._pad
+        if self.output == "replicated-async":
+            # the all-gather runs on NCCL's stream and overlaps whatever the
+            # caller launches next; wait() before reading out_full
+            self._pending = dist.all_gather_into_tensor(out_full, src, group=self.group, async_op=True)
+        else:
+            dist.all_gather_into_tensor(out_full, src, group=self.group)
         mark("gather")
         return out_full[: self.d]
+
+    def wait(self):
+        """Make the current stream wait for a pending "replicated-async" gather."""
+        if getattr(self, "_pending", None) is not None:
+            self._pending.wait()
+            self._pending = None
 
     def _aggregate_fused(self, rows_local, dev, mark):
         buf, handle, extra = self._fused_buffers(dev)

@@ -142,3 +142,18 @@ def test_bcast_entry_points_check_their_extra_outputs(gl):
     code = gl.lib.gar_combine_bcast(gl.rule_id("median"), ptrs, n, 1, 0, 100, ctypes.c_void_p(0x1000),
                                     ctypes.c_void_p(0x10_0000), arr, 1, None)
     assert code == 5                               # combine is for the Krum family
+
+
+def test_mcast_entry_points_check_their_destination(gl):
+    n = 5
+    ptrs = (ctypes.c_void_p * n)(*[0x20_0000 + 0x1000 * i for i in range(n)])
+
+    def agg(mc):
+        return gl.lib.gar_aggregate_mcast(gl.rule_id("median"), ptrs, n, 1, 0, 100, ctypes.c_void_p(0x10_0000),
+                                          ctypes.c_void_p(mc), None, None, 0, None)
+    assert agg(0) == 1                             # null multicast address
+    assert agg(0x40_0000 + 8) == 4                 # misaligned
+    assert agg(0x40_0000) in (1, 7)                # valid: reaches the device check (no GPU here)
+    code = gl.lib.gar_combine_mcast(gl.rule_id("median"), ptrs, n, 1, 0, 100, ctypes.c_void_p(0x1000),
+                                    ctypes.c_void_p(0x10_0000), ctypes.c_void_p(0x40_0000), None)
+    assert code == 5                               # combine is for the Krum family

@@ -70,6 +70,10 @@ def _worker(rank, world, port, x, f, results):
         assert (agg.lo, agg.hi) == (lo, hi)
         full = agg.aggregate(local)
         out[rule] = (full.numpy().copy(), None if agg.selected is None else agg.selected.numpy().copy())
+        agg_async = ShardedAggregator(rule, n, f, d, backend=be, output="replicated-async")
+        full_async = agg_async.aggregate(local)
+        agg_async.wait()
+        assert np.array_equal(full_async.numpy(), out[rule][0])
     results[rank] = out
     dist.destroy_process_group()
 

@@ -1,5 +1,6 @@
-"""torchrun check: the fused output all-gather (symmetric memory + gar_*_bcast)
-gives bit-identical replicated outputs to the NCCL all-gather path, on every rank."""
+"""torchrun check: the fused output all-gather (symmetric memory; multicast
+gar_*_mcast and peer-store gar_*_bcast) gives bit-identical replicated outputs
+to the NCCL all-gather path, on every rank."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, torch.distributed as dist
@@ -16,13 +17,14 @@ X = synth.make_gradients(n, f, hi - lo, seed=11 + rank, device=dev)
 bad = 0
 for rule in ("average", "median", "trimmed_mean", "krum", "multi_krum", "bulyan"):
     a = ShardedAggregator(rule, n, f, d, output="replicated").aggregate(X).clone()
-    fu = ShardedAggregator(rule, n, f, d, output="fused")
-    for _ in range(2):
-        b = fu.aggregate(X).clone()
-    torch.cuda.synchronize()
-    same = torch.equal(a.view(torch.int32), b.view(torch.int32))
-    bad += 0 if same else 1
-    print(f"rank {rank} {rule}: fused == replicated: {same}", flush=True)
+    for mode in ("fused", "fused-p2p"):
+        fu = ShardedAggregator(rule, n, f, d, output=mode)
+        for _ in range(2):
+            b = fu.aggregate(X).clone()
+        torch.cuda.synchronize()
+        same = torch.equal(a.view(torch.int32), b.view(torch.int32))
+        bad += 0 if same else 1
+        print(f"rank {rank} {rule}: {mode} ({fu.fused_path}) == replicated: {same}", flush=True)
 dist.barrier()
 dist.destroy_process_group()
 sys.exit(1 if bad else 0)

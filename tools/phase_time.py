@@ -28,7 +28,8 @@ res = {}
 ws = torch.empty(gar.gar_workspace_bytes("bulyan", n, f, d), dtype=torch.uint8, device="cuda")
 G = torch.empty((n, n), dtype=torch.float64, device="cuda")
 res["gram"] = timed(lambda: gar.gar_gram_partial(X, G, ws, d=d))
-for rule in ("krum", "multi_krum", "bulyan"):
+order = ("krum", "multi_krum", "bulyan") if os.environ.get("ORDER") != "rev" else ("bulyan", "multi_krum", "krum")
+for rule in order:
     agg = gar.init(rule, n, f)
     idx = agg.select(X).clone()
     m = agg.m if hasattr(agg, "m") else 0
@@ -36,4 +37,10 @@ for rule in ("krum", "multi_krum", "bulyan"):
     res[f"select_from_gram_{rule}"] = timed(lambda: gar.gar_select_from_gram(rule, G, n, f, m, idx))
     res[f"select_{rule}"] = timed(lambda: agg.select(X))
     res[f"aggregate_{rule}"] = timed(lambda: agg.aggregate(X, out=out, d=d))
+
+    def chain(rule=rule, m=m, idx=idx):
+        gar.gar_gram_partial(X, G, ws, d=d)
+        gar.gar_select_from_gram(rule, G, n, f, m, idx)
+        gar.gar_combine(rule, X, f, m, idx, out, d=d)
+    res[f"chain_{rule}"] = timed(chain)
 print(json.dumps({"workload": wl, "env": {k: v for k, v in os.environ.items() if k.startswith("GAR_")}, "ms": res}))
