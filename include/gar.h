@@ -176,6 +176,16 @@ gar_status gar_combine_mcast(gar_rule rule, const float* const* grads, int n, in
                              int64_t d_local, const int32_t* indices_dev, float* out, float* out_mc,
                              gar_stream_t stream);
 
+/* Trimmed-set membership (verification entry point for row a3, PAPER.md
+ * l.316 footnote; the north_star's bit-exact "trimmed-set membership"): bit i
+ * of mask_dev[k] is set iff input i is among the n - 2f values the trimmed
+ * mean keeps at coordinate k — canonical order (NaN -> +inf, -0 -> +0), ties
+ * to the lower index.  mask_dev: DEVICE uint64[d], 8-byte aligned.  Same
+ * argument checks and quorum (n >= 2f+1) as gar_aggregate with
+ * GAR_TRIMMED_MEAN.  O(n^2) per coordinate: for checking, not the hot path. */
+gar_status gar_trimmed_membership(const float* const* grads, int n, int f, int64_t d,
+                                  uint64_t* mask_dev, gar_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

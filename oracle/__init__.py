@@ -57,6 +57,7 @@ def lib():
             "oracle_average": [f32p, I, L64, f32p, I],
             "oracle_median": [f32p, I, I, L64, f32p, I],
             "oracle_trimmed_mean": [f32p, I, I, L64, f32p, I],
+            "oracle_trimmed_membership": [f32p, I, I, L64, ctypes.POINTER(ctypes.c_uint64), I],
             "oracle_distances": [f32p, I, L64, f64p, I],
             "oracle_krum_scores": [f64p, I, I, f64p],
             "oracle_multi_krum_select": [f64p, I, I, I, i32p],
@@ -125,6 +126,17 @@ def trimmed_mean(x, f, threads=None):
     _check(lib().oracle_trimmed_mean(_p(x, ctypes.c_float), n, f, d, _p(out, ctypes.c_float),
                                      threads or default_threads()), "trimmed_mean")
     return out
+
+
+def trimmed_membership(x, f, threads=None):
+    """uint64[d]: bit i of entry k set iff input i is kept by the trimmed mean at
+    coordinate k (canonical order, ties by index; n <= 64)."""
+    x = _f32(x)
+    n, d = x.shape
+    mask = np.empty(d, np.uint64)
+    _check(lib().oracle_trimmed_membership(_p(x, ctypes.c_float), n, f, d, _p(mask, ctypes.c_uint64),
+                                           threads or default_threads()), "trimmed_membership")
+    return mask
 
 
 def distances(x, threads=None):

@@ -82,6 +82,23 @@ def trimmed_mean(x, f):
     return out
 
 
+def trimmed_membership(x, f):
+    """Rank counting instead of sorting: input i is kept at coordinate k iff
+    f <= #{j : (c_j, j) < (c_i, i)} < n - f (canonical values, ties by index)."""
+    x = np.asarray(x, np.float32)
+    n, d = x.shape
+    out = np.zeros(d, np.uint64)
+    for k in range(d):
+        c = [_canon(x[i, k]) for i in range(n)]
+        m = 0
+        for i in range(n):
+            rank = sum(1 for j in range(n) if c[j] < c[i] or (c[j] == c[i] and j < i))
+            if f <= rank < n - f:
+                m |= 1 << i
+        out[k] = m
+    return out
+
+
 def distances(x):
     """Exact squared Euclidean distances (Fraction), then rounded to fp64;
     non-finite or > FLT_MAX -> +inf (R4)."""

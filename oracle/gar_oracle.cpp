@@ -168,6 +168,26 @@ int oracle_trimmed_mean(const float* x, int n, int f, int64_t d, float* out, int
   return 0;
 }
 
+// Trimmed-set membership (north_star: bit-exact "trimmed-set membership"):
+// mask[k] bit i set iff input i is among the kept n - 2f at coordinate k, i.e.
+// its position in the canonical order with ties by index (R1, R5) is in
+// [f, n - f).  n <= 64 (one uint64 per coordinate).
+int oracle_trimmed_membership(const float* x, int n, int f, int64_t d, uint64_t* mask, int threads) {
+  if (!x || !mask || n < 1 || n > 64 || f < 0 || d < 0) return 1;
+  if (n < 2 * f + 1) return 2;
+  parallel_coords(d, threads, [&](int64_t lo, int64_t hi) {
+    std::vector<Keyed> v(n);
+    for (int64_t k = lo; k < hi; ++k) {
+      for (int i = 0; i < n; ++i) v[i] = {canon(x[int64_t(i) * d + k]), i};
+      std::sort(v.begin(), v.end(), key_less);
+      uint64_t m = 0;
+      for (int t = f; t < n - f; ++t) m |= uint64_t(1) << v[t].idx;
+      mask[k] = m;
+    }
+  });
+  return 0;
+}
+
 // ---- Pairwise squared distances (the "distances" of Multi-Krum's score,
 // PAPER.md l.210; squared Euclidean per R4) ----------------------------------
 // D[i][j] = sum_k (x_ik - x_jk)^2 in fp64 from the raw fp32 inputs, summed in

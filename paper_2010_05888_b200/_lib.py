@@ -56,6 +56,7 @@ def _load():
         "gar_combine_bcast": ([I, PP, I, I, I, I64, P, P, PP, I, P], I),
         "gar_aggregate_mcast": ([I, PP, I, I, I, I64, P, P, P, P, SZ, P], I),
         "gar_combine_mcast": ([I, PP, I, I, I, I64, P, P, P, P], I),
+        "gar_trimmed_membership": ([PP, I, I, I64, P, P], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -268,3 +269,12 @@ def gar_combine_mcast(rule, grads, f: int, m: int, indices: torch.Tensor, out: t
     check(lib.gar_combine_mcast(rule_id(rule), arr, n, f, m, d, _ptr(indices), _ptr(out), ctypes.c_void_p(out_mc),
                                 stream_handle(dev, stream)), "gar_combine_mcast")
     return out
+
+
+def gar_trimmed_membership(grads, f: int, mask: torch.Tensor, d: int | None = None, stream=None):
+    """mask: device int64[d] (uint64 bit patterns): bit i set iff input i is kept
+    by the trimmed mean at that coordinate."""
+    arr, n, d, dev = row_pointers(grads, d)
+    check(lib.gar_trimmed_membership(arr, n, f, d, _ptr(mask), stream_handle(dev, stream)),
+          "gar_trimmed_membership")
+    return mask

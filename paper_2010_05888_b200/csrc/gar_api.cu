@@ -441,4 +441,16 @@ gar_status gar_combine_mcast(gar_rule rule, const float* const* grads, int n, in
   return combine_impl(rule, grads, n, f, m, d_local, indices_dev, out, extra, stream);
 }
 
+gar_status gar_trimmed_membership(const float* const* grads, int n, int f, int64_t d, uint64_t* mask_dev,
+                                  gar_stream_t stream) {
+  gar_status s = check_rule_args(GAR_TRIMMED_MEAN, n, f, 0);
+  if (s != GAR_OK) return s;
+  if ((s = check_rows(grads, n, d)) != GAR_OK) return s;
+  if (!mask_dev) return GAR_ERR_INVALID_ARGUMENT;
+  if (reinterpret_cast<uintptr_t>(mask_dev) & 7u) return GAR_ERR_ALIGNMENT;
+  if ((s = check_device_rows(grads, n, mask_dev)) != GAR_OK) return s;
+  return cuda_status(gar::launch_trimmed_membership(grads, n, f, d, mask_dev, num_sms(),
+                                                    reinterpret_cast<cudaStream_t>(stream)));
+}
+
 }  // extern "C"

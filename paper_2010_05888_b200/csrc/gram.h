@@ -34,4 +34,8 @@ enum SelectRule { kSelDistancesOnly = 0, kSelMultiKrum = 1, kSelBulyan = 2 };
 cudaError_t launch_select(const double* G, int n, int f, int m, int rule, int32_t* idx_out,
                           double* D_out, cudaStream_t stream);
 
+// Trimmed-set membership masks (membership.cu; verification entry point).
+cudaError_t launch_trimmed_membership(const float* const* rows, int n, int f, int64_t d, uint64_t* mask,
+                                      int num_sms, cudaStream_t stream);
+
 }  // namespace gar

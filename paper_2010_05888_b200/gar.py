@@ -88,6 +88,21 @@ class Aggregator:
         return idx[:nsel]
 
 
+    def aggregate_sharded(self, rows_local, d: int, group=None, output: str = "replicated"):
+        """Multi-GPU form (one process per GPU, d sharded): rows_local is this
+        rank's slice [n, >= d_local] of every gradient (dist.shard_bounds gives
+        the slice); returns the aggregate of the whole d-dimensional vectors,
+        replicated on every rank (or this rank's slice with output="sharded").
+        See dist.ShardedAggregator."""
+        from .dist import ShardedAggregator
+        key = (int(d), id(group), output)
+        sh = getattr(self, "_sharded", {})
+        if key not in sh:
+            sh[key] = ShardedAggregator(self.rule, self.n, self.f, d, m=self.m or None, group=group, output=output)
+            self._sharded = sh
+        return sh[key].aggregate(rows_local)
+
+
 def init(name: str, n: int, f: int, m: int | None = None) -> Aggregator:
     """"The init() function takes the name of the required GAR
     (e.g., "median"), the value of n, the total number of inputs, and f"."""

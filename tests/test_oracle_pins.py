@@ -106,6 +106,32 @@ def test_trimmed_mean_vs_scipy(n, f):
     np.testing.assert_allclose(got, ref, rtol=2e-7, atol=1e-9)
 
 
+def test_trimmed_membership_pins():
+    """north_star: trimmed-set membership.  Pinned to rank counting (brute), to
+    the kept count n - 2f, to f = 0 (everyone kept), and to the trimmed mean
+    itself: the mean of the kept values in ascending order."""
+    rng = np.random.default_rng(5)
+    for n, f in [(1, 0), (5, 1), (7, 3), (11, 2), (31, 7), (64, 15)]:
+        x = rng.integers(-3, 4, (n, 60)).astype(np.float32)       # many ties
+        x[:, ::5] = rng.standard_normal((n, 12)).astype(np.float32)
+        x[0, 3] = np.nan
+        x[n - 1, 7] = -0.0
+        mask = oracle.trimmed_membership(x, f)
+        np.testing.assert_array_equal(mask, brute.trimmed_membership(x, f))
+        counts = [bin(int(m)).count("1") for m in mask]
+        assert counts == [n - 2 * f] * x.shape[1]
+        tm = oracle.trimmed_mean(x, f)
+        for k in range(x.shape[1]):
+            kept = sorted(float(np.float32(np.inf) if np.isnan(x[i, k]) else x[i, k] + np.float32(0))
+                          for i in range(n) if (int(mask[k]) >> i) & 1)
+            s = 0.0
+            for v in kept:
+                s += v
+            assert np.float32(s / len(kept)) == tm[k] or (np.isnan(tm[k]) and np.isnan(s))
+    x = rng.standard_normal((9, 30)).astype(np.float32)
+    assert np.all(oracle.trimmed_membership(x, 0) == np.uint64((1 << 9) - 1))
+
+
 @pytest.mark.parametrize("n,d", [(3, 10), (11, 4099), (31, 9000)])
 def test_distances_vs_scipy(n, d):
     x = rnd(n, d, n + d)

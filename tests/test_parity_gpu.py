@@ -126,6 +126,36 @@ def test_adversarial_values(gar):
                 assert_same_bits(out, oracle.mean_of_rows(x, sel), rule)
 
 
+@pytest.mark.parametrize("n,f", [(1, 0), (5, 1), (7, 3), (11, 2), (19, 4), (31, 7), (33, 8), (64, 15), (64, 31)])
+def test_trimmed_membership(gar, n, f):
+    """north_star: trimmed-set membership bit-exact (gar_trimmed_membership vs
+    the oracle), on tie-heavy and adversarial columns; and the product trimmed
+    mean equals the ascending fp64 mean of the members the mask names."""
+    rng = np.random.default_rng(1000 + n)
+    d = 2 * 1031 + 3
+    x = rng.integers(-3, 4, (n, d)).astype(np.float32)
+    x[:, ::3] = rng.standard_normal((n, len(range(0, d, 3)))).astype(np.float32)
+    x[:, -517:] = synth.adversarial_rows(n, 517, seed=n)
+    X = to_device(x)
+    mask = torch.empty(d, dtype=torch.int64, device="cuda")
+    gar.gar_trimmed_membership(X, f, mask, d=d)
+    out = torch.empty(d, dtype=torch.float32, device="cuda")
+    gar.init("trimmed_mean", n, f).aggregate(X, out=out, d=d)
+    torch.cuda.synchronize()
+    got = mask.cpu().numpy().view(np.uint64)
+    ref = oracle.trimmed_membership(x, f)
+    bad = np.flatnonzero(got != ref)
+    assert bad.size == 0, f"first mismatches at {bad[:5]}: {got[bad[:5]]} vs {ref[bad[:5]]}"
+    res = out.cpu().numpy()
+    canon = np.where(np.isnan(x), np.float32(np.inf), x + np.float32(0))
+    for k in range(0, d, 97):
+        kept = sorted(float(canon[i, k]) for i in range(n) if (int(got[k]) >> i) & 1)
+        s = 0.0
+        for v in kept:
+            s += v
+        assert_same_bits(np.float32(s / len(kept)).reshape(1), res[k:k + 1], f"trimmed mean at {k}")
+
+
 def test_identical_inputs(gar):
     v = np.random.default_rng(3).standard_normal(10_007).astype(np.float32)
     for n in (7, 31, 63):
