@@ -66,22 +66,23 @@ __device__ __forceinline__ float avg_column(const float* col, int R, int stride)
   return static_cast<float>(s / R);
 }
 
-// The networks take values with NaN -> +inf only (fminf), not the full R1
-// canonicalisation: FMNMX orders -0 and +0 as equal, which can only swap
+// The networks take the raw values: their compare-exchange (fminf + max.NaN,
+// networks.cuh) moves a NaN exactly like +inf, so only the outputs a rule
+// uses are mapped NaN -> +inf.  -0 and +0 compare equal, which can only swap
 // zeros; zeros add exactly nothing to an fp64 sum that starts at +0; and
 // Bulyan's closeness |y - med| and its value comparisons treat -0 == +0.
-// The median output is canonicalised, so every result equals that of the
-// canonical inputs.
+// The median output is canonicalised (R1), so every result equals that of
+// the canonical inputs.
 __device__ __forceinline__ float nan_to_inf(float v) { return fminf(v, __int_as_float(0x7f800000)); }
 
 template <int N>
 __device__ __forceinline__ float median_column(float* v) {
   gar_net::median_net<N>(v);
   if constexpr (N % 2 == 1) {
-    return __fadd_rn(v[(N - 1) / 2], 0.0f);
+    return canon(v[(N - 1) / 2]);
   } else {
-    return static_cast<float>((static_cast<double>(__fadd_rn(v[N / 2 - 1], 0.0f)) +
-                               static_cast<double>(__fadd_rn(v[N / 2], 0.0f))) * 0.5);
+    return static_cast<float>((static_cast<double>(canon(v[N / 2 - 1])) + static_cast<double>(canon(v[N / 2]))) *
+                              0.5);
   }
 }
 
@@ -95,7 +96,7 @@ __device__ __forceinline__ double sum_kept(const float* v, int f) {
     if (f != F) return sum_kept<N, F + 1>(v, f);
     double s = 0.0;
 #pragma unroll
-    for (int t = F; t < N - F; ++t) s += static_cast<double>(v[t]);
+    for (int t = F; t < N - F; ++t) s += static_cast<double>(nan_to_inf(v[t]));
     return s;
   }
 }
@@ -139,7 +140,10 @@ __device__ __forceinline__ float bulyan_column(float* v, float* col, int stride,
   const int beta = THETA - 2 * f;
   gar_net::sort_net<THETA>(v);
 #pragma unroll
-  for (int t = 0; t < THETA; ++t) col[t * stride] = v[t];
+  for (int t = 0; t < THETA; ++t) {
+    v[t] = nan_to_inf(v[t]);
+    col[t * stride] = v[t];
+  }
   constexpr int h = (THETA - 1) / 2;
   float med;
   if constexpr (THETA % 2 == 1) {
@@ -192,7 +196,8 @@ __device__ __forceinline__ float bulyan_column_b3(float* v, const float* const* 
   static_assert(THETA % 2 == 1 && THETA >= 5, "beta = 3 window");
   constexpr int h = (THETA - 1) / 2;
   gar_net::window_net<THETA>(v);
-  const float a0 = v[h - 2], a1 = v[h - 1], med = v[h], a3 = v[h + 1], a4 = v[h + 2];
+  const float a0 = nan_to_inf(v[h - 2]), a1 = nan_to_inf(v[h - 1]), med = nan_to_inf(v[h]);
+  const float a3 = nan_to_inf(v[h + 1]), a4 = nan_to_inf(v[h + 2]);
   const float c0 = closeness(a0, med), c1 = closeness(a1, med);
   const float c3 = closeness(a3, med), c4 = closeness(a4, med);
   const int shift = ((c3 < c0) ? 1 : 0) + ((c4 < c1) ? 1 : 0);
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(32 * (W + kProducers), 1) coord_select_kernel(
       } else {
         float v[N > 0 ? N : 1];
 #pragma unroll
-        for (int r = 0; r < N; ++r) v[r] = nan_to_inf(col[r * kTile]);
+        for (int r = 0; r < N; ++r) v[r] = col[r * kTile];
         if constexpr (MODE == kModeMedian) {
           res = median_column<N>(v);
         } else if constexpr (MODE == kModeTrimmed) {
@@ -391,8 +396,6 @@ __global__ void __launch_bounds__(kLdgThreads) coord_ldg_kernel(const __grid_con
       float v[N];
 #pragma unroll
       for (int r = 0; r < N; ++r) v[r] = __ldcs(rowp[r] + k);
-#pragma unroll
-      for (int r = 0; r < N; ++r) v[r] = nan_to_inf(v[r]);
       if constexpr (MODE == kModeMedian) {
         res = median_column<N>(v);
       } else if constexpr (MODE == kModeTrimmed) {

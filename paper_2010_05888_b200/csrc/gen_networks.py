@@ -19,8 +19,12 @@ Emitted functions (all in-place on ``float v[N]``, ascending order):
 * ``gar_net::window_<N>(v)``  — odd N >= 5: v[h-2..h+2] valid and sorted,
   h = (N-1)/2: Bulyan's coordinate phase when beta = 3 (n = 4f+3).
 
-Values must be canonical (no NaN, no -0): the kernel canonicalises first, so
-fminf/fmaxf (FMNMX) implement an exact compare-exchange.
+Compare-exchange = fminf (FMNMX, drops a NaN operand) + max_nan (FMNMX.NAN,
+returns NaN if either operand is NaN).  With these two, a NaN moves through
+the network exactly like +inf (R1: NaN orders as +inf): min(NaN, x) = x,
+max(NaN, x) = NaN, min/max(NaN, NaN) = NaN.  So inputs need no
+canonicalisation; the kernel maps NaN -> +inf only on the outputs it uses.
+-0 and +0 compare equal (they may swap, which no result can observe).
 """
 from __future__ import annotations
 
@@ -228,7 +232,7 @@ def emit(N, fname, positions):
             continue
         nm = f"t{k}"
         names[k] = nm
-        fn = "fminf" if kind == "min" else "fmaxf"
+        fn = "fminf" if kind == "min" else "max_nan"
         lines.append(f"  const float {nm} = {fn}({ref(a)}, {ref(b)});")
     for p in positions:
         lines.append(f"  v[{p}] = {ref(final[p])};")
@@ -242,9 +246,16 @@ def trim_f(N):
 
 def main(out_path):
     parts = ["// GENERATED by gen_networks.py — do not edit.  Product code (libgar);",
-             "// shares nothing with oracle/.  Pruned Batcher / bitonic networks with",
-             "// +inf padding constant-propagated (DESIGN.md §5, coord_select).",
-             "#pragma once", "namespace gar_net {"]
+             "// shares nothing with oracle/.  Pruned Batcher / bitonic / pairwise /",
+             "// merge-exchange networks with +inf padding constant-propagated",
+             "// (DESIGN.md §4.1, coord_select).",
+             "#pragma once", "namespace gar_net {",
+             "// NaN-propagating max (PTX max.NaN): NaN behaves as +inf in the networks.",
+             "__device__ __forceinline__ float max_nan(float a, float b) {",
+             "  float r;",
+             "  asm(\"max.NaN.f32 %0, %1, %2;\" : \"=f\"(r) : \"f\"(a), \"f\"(b));",
+             "  return r;",
+             "}"]
     table = []
     for N in range(1, MAXN + 1):
         src, c_sort = emit(N, "sort", list(range(N)))
