@@ -176,6 +176,25 @@ gar_status gar_combine_mcast(gar_rule rule, const float* const* grads, int n, in
                              int64_t d_local, const int32_t* indices_dev, float* out, float* out_mc,
                              gar_stream_t stream);
 
+/* d-sharded Gram exchange without a collective library (row a10, PAPER.md
+ * l.437-438): the Gram partial of this rank's slice (as gar_gram_partial),
+ * stored into slot `rank` of every rank's slot array over NVLink, then a
+ * flag handshake, then gram_dev = the sum of the `world` slots in rank order
+ * — the whole-vector Gram matrix, bit-identical on every rank.
+ * peer_slots: host array [world] of the slot arrays (DEVICE fp64
+ *   [world][n*n], 8-byte aligned) of every rank as mapped on this GPU (e.g.
+ *   torch symmetric memory); the caller alternates two slot arrays between
+ *   consecutive calls (a rank may run one call ahead of another).
+ * peer_flags: host array [world] of every rank's flag array (uint32[world],
+ *   zero before the first call, 4-byte aligned).
+ * epoch: > the previous call's epoch, the same on every rank for one call.
+ * world <= 8.  A rank that does not arrive within ~10 s yields NaN in
+ * gram_dev instead of a hang.  workspace as for gar_gram_partial. */
+gar_status gar_gram_exchange(const float* const* grads, int n, int64_t d_local,
+                             double* const* peer_slots, uint32_t* const* peer_flags, int rank,
+                             int world, uint32_t epoch, double* gram_dev, void* workspace,
+                             size_t workspace_bytes, gar_stream_t stream);
+
 /* Trimmed-set membership (verification entry point for row a3, PAPER.md
  * l.316 footnote; the north_star's bit-exact "trimmed-set membership"): bit i
  * of mask_dev[k] is set iff input i is among the n - 2f values the trimmed

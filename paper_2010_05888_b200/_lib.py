@@ -57,6 +57,7 @@ def _load():
         "gar_aggregate_mcast": ([I, PP, I, I, I, I64, P, P, P, P, SZ, P], I),
         "gar_combine_mcast": ([I, PP, I, I, I, I64, P, P, P, P], I),
         "gar_trimmed_membership": ([PP, I, I, I64, P, P], I),
+        "gar_gram_exchange": ([PP, I, I64, PP, PP, I, I, ctypes.c_uint32, P, P, SZ, P], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -278,3 +279,16 @@ def gar_trimmed_membership(grads, f: int, mask: torch.Tensor, d: int | None = No
     check(lib.gar_trimmed_membership(arr, n, f, d, _ptr(mask), stream_handle(dev, stream)),
           "gar_trimmed_membership")
     return mask
+
+
+def gar_gram_exchange(grads, gram: torch.Tensor, workspace: torch.Tensor, peer_slots, peer_flags, rank: int,
+                      world: int, epoch: int, d: int | None = None, stream=None):
+    """Whole-vector Gram matrix of d-sharded rows, exchanged over peer memory
+    (ints peer_slots / peer_flags: every rank's slot / flag arrays)."""
+    arr, n, d, dev = row_pointers(grads, d)
+    sl, _ = _ptr_array(peer_slots)
+    fl, _ = _ptr_array(peer_flags)
+    check(lib.gar_gram_exchange(arr, n, d, sl, fl, rank, world, epoch, _ptr(gram), _ptr(workspace),
+                                workspace.numel() * workspace.element_size(), stream_handle(dev, stream)),
+          "gar_gram_exchange")
+    return gram

@@ -1,0 +1,105 @@
+// exchange.cu — the d-sharded Krum-family exchange (row a10, PAPER.md
+// l.437-438) fused into peer-memory kernels instead of an NCCL all-reduce:
+// every rank reduces its per-CTA partial Gram matrices, stores the result
+// into its own slot of EVERY rank's slot array (NVLink peer stores into
+// symmetric memory), signals each rank's flag with a system-scope release,
+// waits (acquire) until all ranks' flags carry this call's epoch, and sums
+// the world slots in rank order.  Every rank therefore holds the bit-identical
+// whole-vector Gram matrix, and no collective library call sits on the path.
+#include <cstdint>
+
+#include "common.cuh"
+#include "gram.h"
+
+namespace gar {
+
+namespace {
+
+// G_local = sum of the CTA partials (same fixed order as gram_reduce_kernel:
+// 8 strided groups, then the 8 group sums), stored at slot `rank` of every
+// rank's slot array.
+__global__ void __launch_bounds__(256) gram_reduce_bcast_kernel(const double* __restrict__ partials, int n_parts,
+                                                                int nn, PeerSlots slots, int world, int rank) {
+  __shared__ double red[8][33];
+  const int e = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int g = threadIdx.x >> 5;
+  double s = 0.0;
+  if (e < nn)
+    for (int p = g; p < n_parts; p += 8) s += partials[static_cast<size_t>(p) * nn + e];
+  red[g][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (threadIdx.x < 32 && e < nn) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += red[q][threadIdx.x];
+    for (int r = 0; r < world; ++r) slots.p[r][static_cast<size_t>(rank) * nn + e] = t;
+  }
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Block 0 publishes this rank's slot writes (they completed with the previous
+// kernel) to every rank's flag[rank]; every block then waits until all
+// `world` local flags reach `epoch` and sums the slots in rank order.  A wait
+// longer than ~10 s (a rank that never arrives) gives up and yields NaN
+// instead of hanging the GPU.
+__global__ void __launch_bounds__(256) gram_gather_kernel(PeerFlags flags, int world, int rank, uint32_t epoch,
+                                                          const double* __restrict__ local_slots, int nn,
+                                                          double* __restrict__ G) {
+  __shared__ int ok;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int r = 0; r < world; ++r) st_release_sys(flags.p[r] + rank, epoch);
+  }
+  if (threadIdx.x == 0) {
+    const uint32_t* mine = flags.p[rank];
+    const uint64_t t0 = global_ns();
+    int good = 1;
+    for (int r = 0; r < world; ++r) {
+      while (static_cast<int32_t>(ld_acquire_sys(mine + r) - epoch) < 0) {
+        if (global_ns() - t0 > 10000000000ull) {
+          good = 0;
+          break;
+        }
+        __nanosleep(100);
+      }
+      if (!good) break;
+    }
+    ok = good;
+  }
+  __syncthreads();
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nn) return;
+  double s = 0.0;
+  for (int r = 0; r < world; ++r) s += local_slots[static_cast<size_t>(r) * nn + e];
+  G[e] = ok ? s : __longlong_as_double(0x7ff8000000000000ll);
+}
+
+}  // namespace
+
+cudaError_t launch_gram_exchange(const double* partials, int n_parts, int n, const PeerSlots& slots,
+                                 const PeerFlags& flags, int world, int rank, uint32_t epoch, double* G,
+                                 cudaStream_t stream) {
+  const int nn = n * n;
+  gram_reduce_bcast_kernel<<<(nn + 31) / 32, 256, 0, stream>>>(partials, n_parts, nn, slots, world, rank);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  gram_gather_kernel<<<(nn + 255) / 256, 256, 0, stream>>>(flags, world, rank, epoch, slots.p[rank], nn, G);
+  return cudaGetLastError();
+}
+
+}  // namespace gar

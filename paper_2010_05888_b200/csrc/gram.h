@@ -34,6 +34,19 @@ enum SelectRule { kSelDistancesOnly = 0, kSelMultiKrum = 1, kSelBulyan = 2 };
 cudaError_t launch_select(const double* G, int n, int f, int m, int rule, int32_t* idx_out,
                           double* D_out, cudaStream_t stream);
 
+// Peer-memory Gram exchange (exchange.cu): slot arrays double[world][n*n]
+// and flag arrays uint32[world] of every rank, as mapped on this GPU.
+constexpr int kMaxWorld = 8;
+struct PeerSlots {
+  double* p[kMaxWorld];
+};
+struct PeerFlags {
+  uint32_t* p[kMaxWorld];
+};
+cudaError_t launch_gram_exchange(const double* partials, int n_parts, int n, const PeerSlots& slots,
+                                 const PeerFlags& flags, int world, int rank, uint32_t epoch, double* G,
+                                 cudaStream_t stream);
+
 // Trimmed-set membership masks (membership.cu; verification entry point).
 cudaError_t launch_trimmed_membership(const float* const* rows, int n, int f, int64_t d, uint64_t* mask,
                                       int num_sms, cudaStream_t stream);

@@ -8,12 +8,15 @@ coordinates).  Then:
 * Average / Median / trimmed mean and the Bulyan coordinate phase are purely
   per-coordinate: each rank aggregates its own slice, no communication;
 * Krum / Multi-Krum / Bulyan need the n x n distance matrix of the WHOLE
-  vectors: each rank computes the partial Gram matrix of its slice
-  (``gar_gram_partial``), one all-reduce (SUM, fp64, n*n*8 <= 32 KB) over NCCL
-  sums them (the centring of the Gram is per coordinate, so partial Grams of
-  disjoint slices add up exactly), every rank runs the identical deterministic
-  selection (``gar_select_from_gram``) and combines its own slice
-  (``gar_combine``);
+  vectors: each rank computes the partial Gram matrix of its slice and the
+  ranks sum them (the centring of the Gram is per coordinate, so partial
+  Grams of disjoint slices add up exactly).  By default the sum is fused into
+  the Gram's own kernels over NVLink peer memory (``gar_gram_exchange``: the
+  reduced partial is stored into every rank's symmetric slot array, a flag
+  handshake, a rank-ordered sum -- no collective library call); or
+  ``gar_gram_partial`` + one NCCL all-reduce (``exchange="nccl"``).  Every
+  rank then runs the identical deterministic selection
+  (``gar_select_from_gram``) and combines its own slice (``gar_combine``);
 * the aggregate is all-gathered (``output="replicated"``: NCCL all-gather
   after the kernel, the north_star default), written by the producing kernel
   itself into every GPU's output buffer over NVLink (``output="fused"``:
@@ -69,6 +72,9 @@ class _LibgarBackend:
     def select_from_gram(self, rule, gram, n, f, m, idx):
         return self._lib.gar_select_from_gram(rule, gram, n, f, m, idx)
 
+    def gram_exchange(self, rows, gram, ws, d, slots, flags, rank, world, epoch):
+        self._lib.gar_gram_exchange(rows, gram, ws, slots, flags, rank, world, epoch, d=d)
+
     def combine(self, rule, rows, f, m, idx, out, d, extra=()):
         if isinstance(extra, Multicast):
             self._lib.gar_combine_mcast(rule, rows, f, m, idx, out, extra.addr, d=d)
@@ -100,7 +106,7 @@ class ShardedAggregator:
     process group: one process per GPU, each holding its slice of every row."""
 
     def __init__(self, rule: str, n: int, f: int, d: int, m: int | None = None, group=None,
-                 output: str = "replicated", backend=None):
+                 output: str = "replicated", backend=None, exchange: str = "auto"):
         if output not in ("replicated", "replicated-async", "sharded", "fused", "fused-mc"):
             raise ValueError(output)
         self.rule, self.n, self.f, self.d = rule, int(n), int(f), int(d)
@@ -113,6 +119,14 @@ class ShardedAggregator:
         self.per = shard_len(self.d, self.world)
         self.output = output
         self.backend = backend if backend is not None else _LibgarBackend()
+        # Krum-family Gram exchange: "peer" = gar_gram_exchange over symmetric
+        # memory (one fused reduce + peer stores + flag handshake, no NCCL),
+        # "nccl" = gar_gram_partial + NCCL all-reduce; "auto" = peer when the
+        # backend has it and the group is on CUDA devices.
+        if exchange not in ("auto", "peer", "nccl"):
+            raise ValueError(exchange)
+        self.exchange = exchange
+        self._xchg = None          # (symmetric buffer, handle, epoch) for the peer exchange
         self._agg = None
         self._ws = None
         self._gram = None
@@ -139,6 +153,50 @@ class ShardedAggregator:
                 extra = [int(handle.buffer_ptrs[r]) + 4 * self.lo for r in range(self.world) if r != self.rank]
             self._symm = (buf, handle, extra)
         return self._symm
+
+    def _use_peer_exchange(self, device) -> bool:
+        if self.world <= 1 or self.rule not in KRUM_FAMILY or device.type != "cuda":
+            return False
+        if self.exchange == "nccl" or not hasattr(self.backend, "gram_exchange"):
+            return False
+        return True
+
+    def _exchange_buffers(self, device):
+        """Symmetric buffer: two slot arrays fp64[world][n*n] (alternating per
+        call) and the flag array uint32[world]; zeroed and fenced by a barrier
+        once."""
+        if self._xchg is None:
+            import torch.distributed._symmetric_memory as symm_mem
+            nn = self.n * self.n
+            slot_bytes = self.world * nn * 8
+            nbytes = 2 * slot_bytes + 4 * self.world + 16
+            buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+            group = self.group if self.group is not None else dist.group.WORLD
+            handle = symm_mem.rendezvous(buf, group)
+            buf.zero_()
+            handle.barrier()
+            bases = [int(handle.buffer_ptrs[r]) for r in range(self.world)]
+            self._xchg = {"buf": buf, "handle": handle, "bases": bases, "slot_bytes": slot_bytes, "epoch": 0}
+        return self._xchg
+
+    def _gram_whole(self, rows_local, dev, mark):
+        """Whole-vector Gram matrix on every rank (self._gram)."""
+        if self._use_peer_exchange(dev):
+            x = self._exchange_buffers(dev)
+            x["epoch"] += 1
+            par = x["epoch"] % 2
+            slots = [b + par * x["slot_bytes"] for b in x["bases"]]
+            flags = [b + 2 * x["slot_bytes"] for b in x["bases"]]
+            self.backend.gram_exchange(rows_local, self._gram, self._ws, self.d_local, slots, flags, self.rank,
+                                       self.world, x["epoch"])
+            mark("gram")
+            mark("exchange")
+            return
+        self.backend.gram_partial(rows_local, self._gram, self._ws, self.d_local)
+        mark("gram")
+        if self.world > 1:
+            dist.all_reduce(self._gram, op=dist.ReduceOp.SUM, group=self.group)
+        mark("exchange")
 
     @property
     def fused_path(self) -> str | None:
@@ -176,11 +234,7 @@ class ShardedAggregator:
         if out_local is None:
             out_local = torch.empty(self.d_local, dtype=torch.float32, device=dev)
         if self.rule in KRUM_FAMILY:
-            self.backend.gram_partial(rows_local, self._gram, self._ws, self.d_local)
-            mark("gram")
-            if self.world > 1:
-                dist.all_reduce(self._gram, op=dist.ReduceOp.SUM, group=self.group)
-            mark("exchange")
+            self._gram_whole(rows_local, dev, mark)
             self.backend.select_from_gram(self.rule, self._gram, self.n, self.f, self.m, self._idx)
             mark("select")
             self.backend.combine(self.rule, rows_local, self.f, self.m, self._idx, out_local, self.d_local)
@@ -217,10 +271,7 @@ class ShardedAggregator:
         buf, handle, extra = self._fused_buffers(dev)
         out_local = buf[self.lo: self.hi]
         if self.rule in KRUM_FAMILY:
-            self.backend.gram_partial(rows_local, self._gram, self._ws, self.d_local)
-            mark("gram")
-            dist.all_reduce(self._gram, op=dist.ReduceOp.SUM, group=self.group)
-            mark("exchange")
+            self._gram_whole(rows_local, dev, mark)
             self.backend.select_from_gram(self.rule, self._gram, self.n, self.f, self.m, self._idx)
             mark("select")
             self.backend.combine(self.rule, rows_local, self.f, self.m, self._idx, out_local, self.d_local, extra)

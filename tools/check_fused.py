@@ -16,15 +16,15 @@ lo, hi = shard_bounds(d, rank, world)
 X = synth.make_gradients(n, f, hi - lo, seed=11 + rank, device=dev)
 bad = 0
 for rule in ("average", "median", "trimmed_mean", "krum", "multi_krum", "bulyan"):
-    a = ShardedAggregator(rule, n, f, d, output="replicated").aggregate(X).clone()
-    for mode in ("fused", "fused-p2p"):
-        fu = ShardedAggregator(rule, n, f, d, output=mode)
+    a = ShardedAggregator(rule, n, f, d, output="replicated", exchange="nccl").aggregate(X).clone()
+    for mode, exch in (("replicated", "peer"), ("fused", "peer"), ("fused", "nccl"), ("fused-mc", "peer")):
+        fu = ShardedAggregator(rule, n, f, d, output=mode, exchange=exch)
         for _ in range(2):
             b = fu.aggregate(X).clone()
         torch.cuda.synchronize()
         same = torch.equal(a.view(torch.int32), b.view(torch.int32))
         bad += 0 if same else 1
-        print(f"rank {rank} {rule}: {mode} ({fu.fused_path}) == replicated: {same}", flush=True)
+        print(f"rank {rank} {rule}: {mode} ({fu.fused_path}) exchange={exch} == replicated/nccl: {same}", flush=True)
 dist.barrier()
 dist.destroy_process_group()
 sys.exit(1 if bad else 0)
