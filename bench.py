@@ -180,9 +180,12 @@ def run_ours(args):
         return e
 
     def step(record):
+        # fused output: one cross-GPU barrier per step (the last rule's), which
+        # makes all six replicated outputs readable (dist.ShardedAggregator.sync)
         for r in RULES:
+            last_rule = r == RULES[-1]
             if not record:
-                aggs[r].aggregate(X, out_local=outs[r], out_full=full[r])
+                aggs[r].aggregate(X, out_local=outs[r], out_full=full[r], barrier=last_rule)
                 continue
             last = [ev()]
 
@@ -190,7 +193,7 @@ def run_ours(args):
                 e = ev()
                 segs.append((CLASS[label], r, last[0], e))
                 last[0] = e
-            aggs[r].aggregate(X, out_local=outs[r], out_full=full[r], mark=mark)
+            aggs[r].aggregate(X, out_local=outs[r], out_full=full[r], mark=mark, barrier=last_rule)
         for r in RULES:              # output="replicated-async": the step ends when every gather has
             aggs[r].wait()           # landed (they overlap the following rules' kernels)
 
@@ -257,7 +260,8 @@ def run_ours(args):
             for r in RULES:
                 if r in rule_drained:              # fused outputs live in the aggregator's own buffer
                     stream.wait_event(rule_drained[r])
-                res = aggs[r].aggregate(xbuf[bb], out_local=obuf[bb][r], out_full=fbuf[bb][r])
+                res = aggs[r].aggregate(xbuf[bb], out_local=obuf[bb][r], out_full=fbuf[bb][r],
+                                        barrier=r == RULES[-1])
                 aggs[r].wait()
                 local_res = res[lo:hi] if res.numel() > dl else res
                 done = torch.cuda.Event()

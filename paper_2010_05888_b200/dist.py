@@ -143,16 +143,24 @@ class ShardedAggregator:
         measured slower than the peer stores on B200, profiles/)."""
         if self._symm is None:
             import torch.distributed._symmetric_memory as symm_mem
-            buf = symm_mem.empty(self.per * self.world, dtype=torch.float32, device=device)
+            # two output buffers, alternating per call, so a deferred barrier
+            # (aggregate(barrier=False) + sync()) cannot let a rank that runs
+            # one call ahead overwrite an output another rank may still read
+            bufs = []
             group = self.group if self.group is not None else dist.group.WORLD
-            handle = symm_mem.rendezvous(buf, group)
-            mc = int(handle.multicast_ptr or 0)
-            if mc and self.output == "fused-mc":
-                extra = Multicast(mc + 4 * self.lo)
-            else:
-                extra = [int(handle.buffer_ptrs[r]) + 4 * self.lo for r in range(self.world) if r != self.rank]
-            self._symm = (buf, handle, extra)
-        return self._symm
+            for _ in range(2):
+                buf = symm_mem.empty(self.per * self.world, dtype=torch.float32, device=device)
+                handle = symm_mem.rendezvous(buf, group)
+                mc = int(handle.multicast_ptr or 0)
+                if mc and self.output == "fused-mc":
+                    extra = Multicast(mc + 4 * self.lo)
+                else:
+                    extra = [int(handle.buffer_ptrs[r]) + 4 * self.lo for r in range(self.world) if r != self.rank]
+                bufs.append((buf, handle, extra))
+            self._symm = bufs
+            self._calls = 0
+        self._calls += 1
+        return self._symm[self._calls % 2]
 
     def _use_peer_exchange(self, device) -> bool:
         if self.world <= 1 or self.rule not in KRUM_FAMILY or device.type != "cuda":
@@ -203,7 +211,7 @@ class ShardedAggregator:
         """"multicast" / "p2p" once the fused buffers exist, else None."""
         if self._symm is None:
             return None
-        return "multicast" if isinstance(self._symm[2], Multicast) else "p2p"
+        return "multicast" if isinstance(self._symm[0][2], Multicast) else "p2p"
 
     # -- lazily created per-device state ------------------------------------------
     def _state(self, device):
@@ -220,17 +228,20 @@ class ShardedAggregator:
             self._agg = init(self.rule, self.n, self.f, self.m or None)
 
     def aggregate(self, rows_local, out_local: torch.Tensor | None = None,
-                  out_full: torch.Tensor | None = None, mark=None) -> torch.Tensor:
+                  out_full: torch.Tensor | None = None, mark=None, barrier: bool = True) -> torch.Tensor:
         """rows_local: [n, >= d_local] slice of the gradients.  Returns the
         local slice (output="sharded") or the whole aggregate (replicated).
         `mark(label)`, if given, is called after each stage ("gram",
         "exchange", "select", "combine", "coord", "gather") — the benchmark
-        records CUDA events there."""
+        records CUDA events there.  Fused outputs: barrier=False skips the
+        cross-GPU barrier that makes the replicated output readable; the
+        caller then calls sync() (any aggregator of the group) before reading
+        it, and reads it before its next sync()."""
         dev = rows_local.device if isinstance(rows_local, torch.Tensor) else rows_local[0].device
         self._state(dev)
         mark = mark or (lambda label: None)
         if self.output in ("fused", "fused-mc") and self.world > 1:
-            return self._aggregate_fused(rows_local, dev, mark)
+            return self._aggregate_fused(rows_local, dev, mark, barrier)
         if out_local is None:
             out_local = torch.empty(self.d_local, dtype=torch.float32, device=dev)
         if self.rule in KRUM_FAMILY:
@@ -267,7 +278,13 @@ class ShardedAggregator:
             self._pending.wait()
             self._pending = None
 
-    def _aggregate_fused(self, rows_local, dev, mark):
+    def sync(self):
+        """Cross-GPU barrier of the fused output: after it, every output
+        written by this group's earlier calls (on every rank) is readable."""
+        if self._symm is not None:
+            self._symm[0][1].barrier()
+
+    def _aggregate_fused(self, rows_local, dev, mark, barrier=True):
         buf, handle, extra = self._fused_buffers(dev)
         out_local = buf[self.lo: self.hi]
         if self.rule in KRUM_FAMILY:
@@ -279,7 +296,8 @@ class ShardedAggregator:
         else:
             self.backend.coordinatewise_bcast(self._agg, rows_local, out_local, self.d_local, extra)
             mark("coord")
-        handle.barrier()        # every rank's slices have landed in every buffer
+        if barrier:
+            handle.barrier()    # every rank's slices have landed in every buffer
         mark("gather")
         return buf[: self.d]
 

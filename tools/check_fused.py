@@ -25,6 +25,18 @@ for rule in ("average", "median", "trimmed_mean", "krum", "multi_krum", "bulyan"
         same = torch.equal(a.view(torch.int32), b.view(torch.int32))
         bad += 0 if same else 1
         print(f"rank {rank} {rule}: {mode} ({fu.fused_path}) exchange={exch} == replicated/nccl: {same}", flush=True)
+# deferred barrier: six calls without a barrier, one sync(), then every output
+aggs = {r: ShardedAggregator(r, n, f, d, output="fused") for r in ("average", "median", "trimmed_mean", "krum",
+                                                                  "multi_krum", "bulyan")}
+refs = {r: ShardedAggregator(r, n, f, d, output="replicated", exchange="nccl").aggregate(X).clone() for r in aggs}
+for _ in range(3):
+    outs = {r: a.aggregate(X, barrier=False) for r, a in aggs.items()}
+    aggs["bulyan"].sync()
+    torch.cuda.synchronize()
+    for r in aggs:
+        same = torch.equal(outs[r].view(torch.int32), refs[r].view(torch.int32))
+        bad += 0 if same else 1
+print(f"rank {rank} deferred-barrier outputs ok: {bad == 0}", flush=True)
 dist.barrier()
 dist.destroy_process_group()
 sys.exit(1 if bad else 0)
