@@ -157,3 +157,20 @@ def test_mcast_entry_points_check_their_destination(gl):
     code = gl.lib.gar_combine_mcast(gl.rule_id("median"), ptrs, n, 1, 0, 100, ctypes.c_void_p(0x1000),
                                     ctypes.c_void_p(0x10_0000), ctypes.c_void_p(0x40_0000), None)
     assert code == 5                               # combine is for the Krum family
+
+
+def test_gram_exchange_checks_its_peer_arrays(gl):
+    n = 5
+    ptrs = (ctypes.c_void_p * n)(*[0x20_0000 + 0x1000 * i for i in range(n)])
+
+    def call(slots, flags, rank, world):
+        sa = (ctypes.c_void_p * max(len(slots), 1))(*slots)
+        fa = (ctypes.c_void_p * max(len(flags), 1))(*flags)
+        return gl.lib.gar_gram_exchange(ptrs, n, 100, sa, fa, rank, world, 1, ctypes.c_void_p(0x50_0000),
+                                        ctypes.c_void_p(0x60_0000), 1 << 30, None)
+    ok_s, ok_f = [0x70_0000, 0x71_0000], [0x72_0000, 0x73_0000]
+    assert call(ok_s, ok_f, 2, 2) == 1                  # rank outside [0, world)
+    assert call(ok_s * 5, ok_f * 5, 0, 10) == 1         # world > 8
+    assert call([0x70_0000, 0], ok_f, 0, 2) == 1         # null slot array
+    assert call([0x70_0004, 0x71_0000], ok_f, 0, 2) == 4  # misaligned slot array
+    assert call(ok_s, ok_f, 1, 2) in (1, 7)             # valid: reaches the device check (no GPU here)
