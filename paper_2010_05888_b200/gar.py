@@ -76,6 +76,26 @@ class Aggregator:
                                              _lib.stream_handle(dev, stream)), f"aggregate[{self.rule}]")
         return out
 
+    def graphed(self, grads, out: torch.Tensor, d: int | None = None, indices: torch.Tensor | None = None):
+        """A CUDA graph of aggregate(grads, out) for fixed buffers: the
+        returned callable replays the whole kernel sequence (Gram, reduction,
+        selection, combine, or the coordinate kernel) with one launch, which
+        is what small, launch-bound configurations (d ~ 1e5) need.  The
+        gradient buffers and `out` must stay allocated and at the same
+        addresses; their contents may change between replays."""
+        self._check_n(grads)
+        dev = grads.device if isinstance(grads, torch.Tensor) else grads[0].device
+        self.aggregate(grads, out=out, d=d, indices=indices)          # warm-up: workspace, attributes, caches
+        torch.cuda.synchronize(dev)
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(graph, stream=side):
+                self.aggregate(grads, out=out, d=d, indices=indices)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        return graph.replay
+
     def select(self, grads, d: int | None = None, stream=None) -> torch.Tensor:
         """Selected input indices (device int32), in selection order."""
         self._check_n(grads)

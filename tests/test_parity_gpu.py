@@ -156,6 +156,22 @@ def test_trimmed_membership(gar, n, f):
         assert_same_bits(np.float32(s / len(kept)).reshape(1), res[k:k + 1], f"trimmed mean at {k}")
 
 
+def test_graphed_aggregate_matches_eager(gar):
+    """Aggregator.graphed: a CUDA graph of the call, replayed on new contents
+    of the same buffers, equals the eager call bit for bit."""
+    n, f, d = 11, 2, 79_510
+    X = to_device(synth.make_gradients(n, f, d, seed=3, ld=d).numpy())
+    for rule in RULES:
+        a = gar.init(rule, n, f)
+        out = torch.empty(d, dtype=torch.float32, device="cuda")
+        replay = a.graphed(X, out, d=d)
+        X.mul_(1.5).add_(0.25)                       # new contents, same addresses
+        replay()
+        ref = a.aggregate(X, out=torch.empty(d, dtype=torch.float32, device="cuda"), d=d)
+        torch.cuda.synchronize()
+        assert_same_bits(out.cpu().numpy(), ref.cpu().numpy(), rule)
+
+
 def test_identical_inputs(gar):
     v = np.random.default_rng(3).standard_normal(10_007).astype(np.float32)
     for n in (7, 31, 63):
