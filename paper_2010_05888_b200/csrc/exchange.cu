@@ -15,25 +15,19 @@ namespace gar {
 
 namespace {
 
-// G_local = sum of the CTA partials (same fixed order as gram_reduce_kernel:
-// 8 strided groups, then the 8 group sums), stored at slot `rank` of every
-// rank's slot array.
+// G_local = sum of the CTA partials (same order as gram_reduce_kernel: one
+// warp per entry, lane-strided sums, xor-shuffle tree), stored at slot `rank`
+// of every rank's slot array.
 __global__ void __launch_bounds__(256) gram_reduce_bcast_kernel(const double* __restrict__ partials, int n_parts,
                                                                 int nn, PeerSlots slots, int world, int rank) {
-  __shared__ double red[8][33];
-  const int e = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int g = threadIdx.x >> 5;
+  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (e >= nn) return;
   double s = 0.0;
-  if (e < nn)
-    for (int p = g; p < n_parts; p += 8) s += partials[static_cast<size_t>(p) * nn + e];
-  red[g][threadIdx.x & 31] = s;
-  __syncthreads();
-  if (threadIdx.x < 32 && e < nn) {
-    double t = 0.0;
+  for (int p = lane; p < n_parts; p += 32) s += partials[static_cast<size_t>(p) * nn + e];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) t += red[q][threadIdx.x];
-    for (int r = 0; r < world; ++r) slots.p[r][static_cast<size_t>(rank) * nn + e] = t;
-  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane < world) slots.p[lane][static_cast<size_t>(rank) * nn + e] = s;
 }
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -95,7 +89,7 @@ cudaError_t launch_gram_exchange(const double* partials, int n_parts, int n, con
                                  const PeerFlags& flags, int world, int rank, uint32_t epoch, double* G,
                                  cudaStream_t stream) {
   const int nn = n * n;
-  gram_reduce_bcast_kernel<<<(nn + 31) / 32, 256, 0, stream>>>(partials, n_parts, nn, slots, world, rank);
+  gram_reduce_bcast_kernel<<<(nn + 7) / 8, 256, 0, stream>>>(partials, n_parts, nn, slots, world, rank);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   gram_gather_kernel<<<(nn + 255) / 256, 256, 0, stream>>>(flags, world, rank, epoch, slots.p[rank], nn, G);

@@ -82,22 +82,19 @@ __global__ void __launch_bounds__(kSimtThreads) gram_simt_kernel(const __grid_co
 }
 
 // 256 threads = 32 entries x 8 partial groups; fixed-order sums.
+// One warp per Gram entry: lane l sums partials l, l+32, ... (independent
+// loads in flight together), then a fixed xor-shuffle tree -- a deterministic
+// order, and latency ~ one memory round trip instead of n_parts/8 dependent ones.
 __global__ void __launch_bounds__(256) gram_reduce_kernel(const double* __restrict__ partials, int n_parts,
                                                           int nn, double* __restrict__ G) {
-  __shared__ double red[8][33];
-  const int e = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int g = threadIdx.x >> 5;
+  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (e >= nn) return;
   double s = 0.0;
-  if (e < nn)
-    for (int p = g; p < n_parts; p += 8) s += partials[static_cast<size_t>(p) * nn + e];
-  red[g][threadIdx.x & 31] = s;
-  __syncthreads();
-  if (threadIdx.x < 32 && e < nn) {
-    double t = 0.0;
+  for (int p = lane; p < n_parts; p += 32) s += partials[static_cast<size_t>(p) * nn + e];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) t += red[q][threadIdx.x];
-    G[e] = t;
-  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) G[e] = s;
 }
 
 }  // namespace
@@ -119,7 +116,7 @@ cudaError_t launch_gram_partials_simt(const float* const* rows, int n, int64_t d
 
 cudaError_t launch_gram_reduce(const double* partials, int n_parts, int n, double* G, cudaStream_t stream) {
   const int nn = n * n;
-  gram_reduce_kernel<<<(nn + 31) / 32, 256, 0, stream>>>(partials, n_parts, nn, G);
+  gram_reduce_kernel<<<(nn + 7) / 8, 256, 0, stream>>>(partials, n_parts, nn, G);
   return cudaGetLastError();
 }
 
