@@ -176,6 +176,22 @@ gar_status gar_combine_mcast(gar_rule rule, const float* const* grads, int n, in
                              int64_t d_local, const int32_t* indices_dev, float* out, float* out_mc,
                              gar_stream_t stream);
 
+/* Fused server step (the update on the far side of the path, PAPER.md
+ * l.122-125, x <- x - gamma * GAR(gradients)):
+ * params[k] <- fma(-lr, GAR(grads)[k], params[k]) with one rounding, applied
+ * by the producing kernel instead of storing the aggregate (saves the
+ * aggregate's write and re-read).  params: DEVICE fp32[d], 16-byte aligned,
+ * in/out, not aliasing the inputs; lr finite.  Otherwise as
+ * gar_aggregate_ex / gar_combine; d-sharded callers pass their parameter
+ * slice (the ZeRO-style consumer of the sharded output). */
+gar_status gar_aggregate_sgd(gar_rule rule, const float* const* grads, int n, int f, int m,
+                             int64_t d, float* params, float lr, int32_t* indices_dev,
+                             void* workspace, size_t workspace_bytes, gar_stream_t stream);
+
+gar_status gar_combine_sgd(gar_rule rule, const float* const* grads, int n, int f, int m,
+                           int64_t d_local, const int32_t* indices_dev, float* params, float lr,
+                           gar_stream_t stream);
+
 /* d-sharded Gram exchange without a collective library (row a10, PAPER.md
  * l.437-438): the Gram partial of this rank's slice (as gar_gram_partial),
  * stored into slot `rank` of every rank's slot array over NVLink, then a

@@ -58,6 +58,7 @@ def lib():
             "oracle_median": [f32p, I, I, L64, f32p, I],
             "oracle_trimmed_mean": [f32p, I, I, L64, f32p, I],
             "oracle_trimmed_membership": [f32p, I, I, L64, ctypes.POINTER(ctypes.c_uint64), I],
+            "oracle_sgd_update": [f32p, f32p, ctypes.c_float, L64, f32p],
             "oracle_distances": [f32p, I, L64, f64p, I],
             "oracle_krum_scores": [f64p, I, I, f64p],
             "oracle_multi_krum_select": [f64p, I, I, I, i32p],
@@ -137,6 +138,16 @@ def trimmed_membership(x, f, threads=None):
     _check(lib().oracle_trimmed_membership(_p(x, ctypes.c_float), n, f, d, _p(mask, ctypes.c_uint64),
                                            threads or default_threads()), "trimmed_membership")
     return mask
+
+
+def sgd_update(params, g, lr):
+    """The server step x - lr * g with one rounding (fma)."""
+    p = _f32(params).reshape(-1)
+    gg = _f32(g).reshape(-1)
+    out = np.empty_like(p)
+    _check(lib().oracle_sgd_update(_p(p, ctypes.c_float), _p(gg, ctypes.c_float), float(lr), p.size,
+                                   _p(out, ctypes.c_float)), "sgd_update")
+    return out
 
 
 def distances(x, threads=None):

@@ -168,6 +168,14 @@ int oracle_trimmed_mean(const float* x, int n, int f, int64_t d, float* out, int
   return 0;
 }
 
+// Server step (x <- x - gamma * GAR(...)), the update the
+// fused kernels apply: out[k] = fma(-lr, g[k], p[k]), one rounding to fp32.
+int oracle_sgd_update(const float* p, const float* g, float lr, int64_t d, float* out) {
+  if (!p || !g || !out || d < 0) return 1;
+  for (int64_t k = 0; k < d; ++k) out[k] = std::fmaf(-lr, g[k], p[k]);
+  return 0;
+}
+
 // Trimmed-set membership (north_star: bit-exact "trimmed-set membership"):
 // mask[k] bit i set iff input i is among the kept n - 2f at coordinate k, i.e.
 // its position in the canonical order with ties by index (R1, R5) is in

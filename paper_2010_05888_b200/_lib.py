@@ -58,6 +58,8 @@ def _load():
         "gar_combine_mcast": ([I, PP, I, I, I, I64, P, P, P, P], I),
         "gar_trimmed_membership": ([PP, I, I, I64, P, P], I),
         "gar_gram_exchange": ([PP, I, I64, PP, PP, I, I, ctypes.c_uint32, P, P, SZ, P], I),
+        "gar_aggregate_sgd": ([I, PP, I, I, I, I64, P, ctypes.c_float, P, P, SZ, P], I),
+        "gar_combine_sgd": ([I, PP, I, I, I, I64, P, P, ctypes.c_float, P], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -292,3 +294,21 @@ def gar_gram_exchange(grads, gram: torch.Tensor, workspace: torch.Tensor, peer_s
                                 workspace.numel() * workspace.element_size(), stream_handle(dev, stream)),
           "gar_gram_exchange")
     return gram
+
+
+def gar_aggregate_sgd(rule, grads, f: int, m: int, params: torch.Tensor, lr: float, indices=None, workspace=None,
+                      d: int | None = None, stream=None):
+    """params <- params - lr * GAR(grads), fused into the producing kernel."""
+    arr, n, d, dev = row_pointers(grads, d)
+    wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    check(lib.gar_aggregate_sgd(rule_id(rule), arr, n, f, m, d, _ptr(params), float(lr), _ptr(indices),
+                                _ptr(workspace), wsb, stream_handle(dev, stream)), "gar_aggregate_sgd")
+    return params
+
+
+def gar_combine_sgd(rule, grads, f: int, m: int, indices: torch.Tensor, params: torch.Tensor, lr: float,
+                    d: int | None = None, stream=None):
+    arr, n, d, dev = row_pointers(grads, d)
+    check(lib.gar_combine_sgd(rule_id(rule), arr, n, f, m, d, _ptr(indices), _ptr(params), float(lr),
+                              stream_handle(dev, stream)), "gar_combine_sgd")
+    return params

@@ -24,11 +24,17 @@ struct RowPtrs {
 // one multimem.st per result is replicated by the NVSwitch into every GPU's
 // buffer, this GPU's included, so each GPU sends its slice over NVLink once
 // instead of once per peer; the local and peer stores are skipped.
+//
+// Or, with sgd set (the fused server step):
+// `out` holds the parameters and each result g updates them in place,
+// out[i] = fma(-lr, g, out[i]) (one rounding), instead of being stored.
 #define GAR_MAX_PEERS 8
 struct OutPtrs {
   float* p[GAR_MAX_PEERS];
   int n;
   float* mc;
+  int sgd;
+  float lr;
 };
 
 __device__ __forceinline__ void mc_store(float* addr, float v) {
@@ -41,13 +47,22 @@ __device__ __forceinline__ void mc_store4(float* addr, float4 v) {
                : "memory");
 }
 
-__device__ __forceinline__ void store_result(float* out, const OutPtrs& extra, int64_t i, float v) {
+// pv: the caller's preloaded out[i] for the fused server step (ignored otherwise).
+__device__ __forceinline__ void store_result(float* out, const OutPtrs& extra, int64_t i, float v, float pv) {
+  if (extra.sgd) {
+    __stcs(out + i, fmaf(-extra.lr, v, pv));
+    return;
+  }
   if (extra.mc) {
     mc_store(extra.mc + i, v);
     return;
   }
   __stcs(out + i, v);
   for (int j = 0; j < extra.n; ++j) extra.p[j][i] = v;
+}
+
+__device__ __forceinline__ void store_result(float* out, const OutPtrs& extra, int64_t i, float v) {
+  store_result(out, extra, i, v, extra.sgd ? __ldcs(out + i) : 0.0f);
 }
 
 // ---------------------------------------------------------------- PTX wrappers

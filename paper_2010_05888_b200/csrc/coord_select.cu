@@ -17,6 +17,13 @@ __global__ void __launch_bounds__(256) copy_row_kernel(const __grid_constant__ R
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n4; q += int64_t(gridDim.x) * blockDim.x) {
     float4 v = __ldcs(reinterpret_cast<const float4*>(src) + q);
     v.x = __fadd_rn(v.x, 0.0f); v.y = __fadd_rn(v.y, 0.0f); v.z = __fadd_rn(v.z, 0.0f); v.w = __fadd_rn(v.w, 0.0f);
+    if (extra.sgd) {
+      float4 w = __ldcs(reinterpret_cast<const float4*>(out) + q);
+      w.x = fmaf(-extra.lr, v.x, w.x); w.y = fmaf(-extra.lr, v.y, w.y);
+      w.z = fmaf(-extra.lr, v.z, w.z); w.w = fmaf(-extra.lr, v.w, w.w);
+      __stcs(reinterpret_cast<float4*>(out) + q, w);
+      continue;
+    }
     if (extra.mc) {
       mc_store4(extra.mc + 4 * q, v);
       continue;

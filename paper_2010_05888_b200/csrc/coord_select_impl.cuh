@@ -325,6 +325,9 @@ __global__ void __launch_bounds__(32 * (W + kProducers), 1) coord_select_kernel(
       for (int r = 0; r < R; ++r) col[r * kTile] = __ldg(rowp[r] + start + c);
     }
     if (c < cnt) {
+      // fused server step: the parameter is loaded before the column work so
+      // its latency overlaps it
+      const float pv = p.extra.sgd ? __ldcs(p.out + start + c) : 0.0f;
       float res;
       if constexpr (MODE == kModeAverage) {
         res = avg_column(col, R, kTile);
@@ -340,7 +343,7 @@ __global__ void __launch_bounds__(32 * (W + kProducers), 1) coord_select_kernel(
           res = bulyan_dispatch<N>(v, col, kTile, p.f, rowp, start + c);
         }
       }
-      store_result(p.out, p.extra, start + c, res);
+      store_result(p.out, p.extra, start + c, res, pv);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
@@ -379,6 +382,7 @@ __global__ void __launch_bounds__(kLdgThreads) coord_ldg_kernel(const __grid_con
   const int64_t d = p.d;
   const int64_t step = int64_t(gridDim.x) * kLdgThreads;
   for (int64_t k = int64_t(blockIdx.x) * kLdgThreads + threadIdx.x; k < d; k += step) {
+    const float pv = p.extra.sgd ? __ldcs(p.out + k) : 0.0f;     // fused server step (see above)
     float res;
     if constexpr (MODE == kModeAverage) {
       double s = 0.0;
@@ -405,7 +409,7 @@ __global__ void __launch_bounds__(kLdgThreads) coord_ldg_kernel(const __grid_con
         res = bulyan_dispatch<N>(v, col, kLdgThreads, p.f, rowp, k);
       }
     }
-    store_result(p.out, p.extra, k, res);
+    store_result(p.out, p.extra, k, res, pv);
   }
 }
 

@@ -2,6 +2,7 @@
 // carving and kernel sequencing.  No arithmetic of the method happens on the
 // host; every step runs in the kernels of coord_select*.cu, gram_*.cu and
 // select.cu.
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -439,6 +440,25 @@ gar_status gar_combine_mcast(gar_rule rule, const float* const* grads, int n, in
   gar_status s = make_mc(out_mc, &extra);
   if (s != GAR_OK) return s;
   return combine_impl(rule, grads, n, f, m, d_local, indices_dev, out, extra, stream);
+}
+
+gar_status gar_aggregate_sgd(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d,
+                             float* params, float lr, int32_t* indices_dev, void* workspace, size_t workspace_bytes,
+                             gar_stream_t stream) {
+  if (!(lr == lr) || lr == INFINITY || lr == -INFINITY) return GAR_ERR_INVALID_ARGUMENT;
+  gar::OutPtrs extra{};
+  extra.sgd = 1;
+  extra.lr = lr;
+  return aggregate_impl(rule, grads, n, f, m, d, params, extra, indices_dev, workspace, workspace_bytes, stream);
+}
+
+gar_status gar_combine_sgd(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d_local,
+                           const int32_t* indices_dev, float* params, float lr, gar_stream_t stream) {
+  if (!(lr == lr) || lr == INFINITY || lr == -INFINITY) return GAR_ERR_INVALID_ARGUMENT;
+  gar::OutPtrs extra{};
+  extra.sgd = 1;
+  extra.lr = lr;
+  return combine_impl(rule, grads, n, f, m, d_local, indices_dev, params, extra, stream);
 }
 
 gar_status gar_gram_exchange(const float* const* grads, int n, int64_t d_local, double* const* peer_slots,

@@ -106,6 +106,37 @@ def test_trimmed_mean_vs_scipy(n, f):
     np.testing.assert_allclose(got, ref, rtol=2e-7, atol=1e-9)
 
 
+def _round_f32(q):
+    """Correctly rounded fp32 of an exact rational (ties to even)."""
+    from fractions import Fraction
+    lo = np.float32(float(q))
+    while Fraction(float(lo)) > q:
+        lo = np.nextafter(lo, np.float32(-np.inf))
+    while Fraction(float(np.nextafter(lo, np.float32(np.inf)))) <= q:
+        lo = np.nextafter(lo, np.float32(np.inf))
+    hi = np.nextafter(lo, np.float32(np.inf))
+    dl, dh = q - Fraction(float(lo)), Fraction(float(hi)) - q
+    if dl < dh or (dl == dh and (int(lo.view(np.uint32)) & 1) == 0):
+        return lo
+    return hi
+
+
+def test_sgd_update_pins():
+    """The fused server step's update, fma(-lr, g, p): exact rational value
+    rounded once to fp32; lr = 0 keeps p; p = g with lr = 1 gives 0."""
+    from fractions import Fraction
+    rng = np.random.default_rng(9)
+    p = (rng.standard_normal(3000) * rng.choice([1e-3, 1.0, 1e3], 3000)).astype(np.float32)
+    g = (rng.standard_normal(3000) * rng.choice([1e-4, 1.0, 1e4], 3000)).astype(np.float32)
+    for lr in (np.float32(0.1), np.float32(1e-3), np.float32(3.0)):
+        got = oracle.sgd_update(p, g, lr)
+        for k in range(0, 3000, 7):
+            exact = Fraction(float(p[k])) - Fraction(float(lr)) * Fraction(float(g[k]))
+            assert got[k] == _round_f32(exact), (k, lr)
+    np.testing.assert_array_equal(oracle.sgd_update(p, g, 0.0), p)
+    assert np.all(oracle.sgd_update(g, g, 1.0) == 0)
+
+
 def test_trimmed_membership_pins():
     """north_star: trimmed-set membership.  Pinned to rank counting (brute), to
     the kept count n - 2f, to f = 0 (everyone kept), and to the trimmed mean

@@ -156,6 +156,36 @@ def test_trimmed_membership(gar, n, f):
         assert_same_bits(np.float32(s / len(kept)).reshape(1), res[k:k + 1], f"trimmed mean at {k}")
 
 
+@pytest.mark.parametrize("n,f,d", [(11, 2, 79_510), (31, 7, 300_001), (64, 15, 20_003)])
+def test_fused_server_step(gar, n, f, d):
+    """gar_aggregate_sgd: params <- fma(-lr, GAR(grads), params) inside the
+    producing kernel equals the oracle's update applied to the (parity-tested)
+    aggregate, bit for bit, for every rule; Krum family also via
+    gar_combine_sgd on the selection."""
+    x = synth.make_gradients(n, f, d, seed=synth.BASE_SEED + 17 + n, ld=d).numpy()
+    X = to_device(x)
+    rng = np.random.default_rng(n)
+    p0 = rng.standard_normal(d).astype(np.float32)
+    lr = np.float32(0.05)
+    for rule in RULES:
+        if rule == "bulyan" and n < 4 * f + 3:
+            continue
+        a = gar.init(rule, n, f)
+        g = a.aggregate(X, out=torch.empty(d, dtype=torch.float32, device="cuda"), d=d)
+        params = torch.from_numpy(p0.copy()).cuda()
+        ws = a.workspace(torch.device("cuda"))
+        gar.gar_aggregate_sgd(rule, X, f, 0, params, float(lr), workspace=ws, d=d)
+        torch.cuda.synchronize()
+        expect = oracle.sgd_update(p0, g.cpu().numpy(), lr)
+        assert_same_bits(params.cpu().numpy(), expect, f"{rule} fused step")
+        if rule in KRUM_FAMILY:
+            idx = a.select(X, d=d)
+            params2 = torch.from_numpy(p0.copy()).cuda()
+            gar.gar_combine_sgd(rule, X, f, 0, idx, params2, float(lr), d=d)
+            torch.cuda.synchronize()
+            assert_same_bits(params2.cpu().numpy(), expect, f"{rule} fused combine step")
+
+
 def test_graphed_aggregate_matches_eager(gar):
     """Aggregator.graphed: a CUDA graph of the call, replayed on new contents
     of the same buffers, equals the eager call bit for bit."""
