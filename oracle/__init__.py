@@ -68,6 +68,8 @@ def lib():
             "oracle_bulyan_coordinate_phase": [f32p, I, I, L64, i32p, I, f32p, I],
             "oracle_multi_krum": [f32p, I, I, I, L64, f32p, i32p, f64p, I],
             "oracle_bulyan": [f32p, I, I, L64, f32p, i32p, f64p, I],
+            "oracle_mda_select": [f64p, I, I, i32p],
+            "oracle_mda": [f32p, I, I, L64, f32p, i32p, f64p, I],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -232,6 +234,28 @@ def multi_krum(x, f, m=None, threads=None, return_D=False):
                                    _p(sel, ctypes.c_int32), _p(D, ctypes.c_double),
                                    threads or default_threads()), "multi_krum")
     return (out, sel, D) if return_D else (out, sel)
+
+
+def mda_select(D, f):
+    """Indices (ascending) of the size n-f subset of minimum diameter
+    (max pairwise squared distance), ties to the lexicographically smallest set."""
+    D = np.ascontiguousarray(D, np.float64)
+    n = D.shape[0]
+    sel = np.empty(max(n - f, 1), np.int32)
+    _check(lib().oracle_mda_select(_p(D, ctypes.c_double), n, f, _p(sel, ctypes.c_int32)), "mda_select")
+    return sel[: n - f]
+
+
+def mda(x, f, threads=None, return_D=False):
+    """MDA: the average of the minimum-diameter subset of n-f inputs."""
+    x = _f32(x)
+    n, d = x.shape
+    out = np.empty(d, np.float32)
+    sel = np.empty(max(n - f, 1), np.int32)
+    D = np.empty((n, n), np.float64)
+    _check(lib().oracle_mda(_p(x, ctypes.c_float), n, f, d, _p(out, ctypes.c_float), _p(sel, ctypes.c_int32),
+                            _p(D, ctypes.c_double), threads or default_threads()), "mda")
+    return (out, sel[: n - f], D) if return_D else (out, sel[: n - f])
 
 
 def krum(x, f, threads=None, return_D=False):

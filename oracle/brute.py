@@ -186,3 +186,20 @@ def multi_krum(x, f, m=None):
     D = distances(x)
     sel, _ = multi_krum_select(D, f, m)
     return mean_of_rows(x, sel), sel
+
+
+def mda(x, f):
+    """Brute force over itertools.combinations with the Euclidean (square-root)
+    diameter, exact fp64 distances from fsum; ties: first in lexicographic order."""
+    import itertools
+    import math
+    x = np.asarray(x, np.float32)
+    n, d = x.shape
+    def dist(i, j):
+        return math.sqrt(math.fsum((float(x[i, k]) - float(x[j, k])) ** 2 for k in range(d)))
+    best, best_set = None, None
+    for s in itertools.combinations(range(n), n - f):
+        diam = max((dist(a, b) for a, b in itertools.combinations(s, 2)), default=0.0)
+        if best is None or diam < best:
+            best, best_set = diam, s
+    return mean_of_rows(x, list(best_set)), np.array(best_set, np.int32)

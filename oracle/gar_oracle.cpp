@@ -387,6 +387,54 @@ int oracle_bulyan(const float* x, int n, int f, int64_t d, float* out, int32_t* 
   return oracle_bulyan_coordinate_phase(x, n, f, d, sel, n - 2 * f, out, threads);
 }
 
+// ---- MDA, Minimum-Diameter Averaging (§3.3 item 3;
+// Rousseeuw, cited there): "finds a subset group of gradients of size q - f
+// with the minimum diameter among all other subsets, where the diameter of a
+// group is defined as the maximum distance between any two gradients of this
+// subset.  MDA then outputs the average of the chosen subset."  Requires
+// q >= 2f + 1 (l.217).  Readings (R13): diameters compare squared
+// distances (the same order as Euclidean, without a square root's rounding);
+// ties go to the lexicographically smallest index set; the
+// average is over the chosen indices in ascending order (R2).  Plain
+// enumeration of every subset of size q - f in lexicographic order.
+int oracle_mda_select(const double* D, int n, int f, int32_t* sel) {
+  if (!D || !sel || n < 1 || n > 64 || f < 0) return 1;
+  if (n < 2 * f + 1) return 2;
+  const int k = n - f;
+  std::vector<int> c(k), best;
+  for (int i = 0; i < k; ++i) c[i] = i;
+  double best_diam = 0.0;
+  bool have = false;
+  while (true) {
+    double diam = 0.0;
+    for (int a = 0; a < k; ++a)
+      for (int b = a + 1; b < k; ++b) diam = std::max(diam, D[int64_t(c[a]) * n + c[b]]);
+    if (!have || diam < best_diam) {   // lexicographic enumeration: the first minimum wins ties
+      best_diam = diam;
+      best = c;
+      have = true;
+    }
+    int i = k - 1;                      // next combination in lexicographic order
+    while (i >= 0 && c[i] == n - k + i) --i;
+    if (i < 0) break;
+    ++c[i];
+    for (int j = i + 1; j < k; ++j) c[j] = c[j - 1] + 1;
+  }
+  for (int i = 0; i < k; ++i) sel[i] = best[i];
+  return 0;
+}
+
+int oracle_mda(const float* x, int n, int f, int64_t d, float* out, int32_t* sel, double* D_out, int threads) {
+  if (!x || !out || !sel || n < 1 || f < 0 || d < 0) return 1;
+  if (n < 2 * f + 1) return 2;
+  std::vector<double> D(int64_t(n) * n);
+  oracle_distances(x, n, d, D.data(), threads);
+  if (D_out) std::memcpy(D_out, D.data(), sizeof(double) * D.size());
+  const int rc = oracle_mda_select(D.data(), n, f, sel);
+  if (rc) return rc;
+  return oracle_mean_of_rows(x, n, d, sel, n - f, out, threads);
+}
+
 // ---- The paper's branch-free 3-element reorder (§4.2) --
 // c = {v0>v1, v0>v2, v1>v2};
 // i0 = (1 + c0 + 2c1 + c2 - (c1 xor c2)) / 2 ; i1 = (4 - c0 - 2c1 - c2 + (c0 xor c1)) / 2

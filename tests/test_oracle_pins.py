@@ -405,3 +405,50 @@ def test_thread_count_does_not_change_results():
                lambda t: oracle.median(x, 3, t)):
         a, b = fn(1), fn(5)
         np.testing.assert_array_equal(a, b)
+
+
+# ---------------------------------------------------------------- MDA
+def test_mda_spec_example():
+    """[(0), (1), (100)], f = 1 -> 0.5 (subset {0, 1}, diameter 1)."""
+    out, sel = oracle.mda(np.array([[0.0], [1.0], [100.0]], np.float32), 1)
+    assert out[0] == np.float32(0.5) and list(sel) == [0, 1]
+
+
+def test_mda_vs_brute_force():
+    """Subset enumeration with squared fp64 distances == itertools brute force
+    with Euclidean (square-root, fsum) distances, on random small inputs."""
+    rng = np.random.default_rng(21)
+    for trial in range(40):
+        n = int(rng.integers(1, 9))
+        f = int(rng.integers(0, (n - 1) // 2 + 1))
+        d = int(rng.integers(1, 5))
+        x = rng.standard_normal((n, d)).astype(np.float32)
+        out, sel = oracle.mda(x, f)
+        bout, bsel = brute.mda(x, f)
+        assert list(sel) == list(bsel), (n, f, sel, bsel)
+        np.testing.assert_array_equal(out, bout)
+
+
+def test_mda_special_cases_and_bounds():
+    rng = np.random.default_rng(22)
+    x = rng.standard_normal((9, 50)).astype(np.float32)
+    np.testing.assert_array_equal(oracle.mda(x, 0)[0], oracle.average(x))         # f = 0: everyone
+    v = rng.standard_normal(30).astype(np.float32)
+    np.testing.assert_array_equal(oracle.mda(np.tile(v, (7, 1)), 3)[0], v)       # identical inputs
+    with pytest.raises(oracle.OracleError):
+        oracle.mda(x, 5)                                                          # q < 2f + 1
+    # Lemma 1 (P:308-312): with at most f Byzantine inputs, the output is within
+    # the correct inputs' diameter of every correct input
+    for trial in range(10):
+        n, f = 11, 3
+        h = (rng.standard_normal((n - f, 40)) * 0.1 + 1.0).astype(np.float32)
+        byz = np.concatenate([-100 * h[:2], rng.standard_normal((1, 40)).astype(np.float32)])
+        xs = np.concatenate([h, byz]).astype(np.float32)
+        perm = rng.permutation(n)
+        out, _ = oracle.mda(xs[perm], f)
+        diam = max(np.linalg.norm(h[i].astype(np.float64) - h[j]) for i in range(n - f) for j in range(n - f))
+        for i in range(n - f):
+            assert np.linalg.norm(out.astype(np.float64) - h[i]) <= diam * (1 + 1e-6)
+        # permutation invariance (no diameter ties with continuous inputs)
+        out2, _ = oracle.mda(xs[rng.permutation(n)], f)
+        np.testing.assert_allclose(out2, out, rtol=1e-6, atol=1e-7)
