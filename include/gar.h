@@ -53,16 +53,18 @@ typedef enum {
   GAR_TRIMMED_MEAN = 2, /* coordinate-wise trimmed mean, l.316 footnote; R6          */
   GAR_KRUM = 3,         /* Multi-Krum with m = 1, l.210-212; R10                     */
   GAR_MULTI_KRUM = 4,   /* average of the m smallest-score inputs, l.210-212         */
-  GAR_BULYAN = 5        /* iterated Krum + coordinate phase, l.219-225; R7, R8       */
+  GAR_BULYAN = 5,       /* iterated Krum + coordinate phase, l.219-225; R7, R8       */
+  GAR_MDA = 6           /* minimum-diameter averaging, l.214-217; R13; q >= 2f+1,   */
+                        /* C(q, f) <= 2^31 (GAR_ERR_UNSUPPORTED above)              */
 } gar_rule;
 
 typedef enum {
   GAR_OK = 0,
   GAR_ERR_INVALID_ARGUMENT = 1, /* null/host pointer, n outside [1,64], f<0, d<0, out aliases an input, bad rule */
-  GAR_ERR_QUORUM = 2,           /* n < 2f+1 (median, trimmed) | 2f+3 (Krum family) | 4f+3 (Bulyan); l.208, l.212, l.225 */
+  GAR_ERR_QUORUM = 2,           /* n < 2f+1 (median, trimmed, MDA) | 2f+3 (Krum family) | 4f+3 (Bulyan); l.208, l.212, l.217, l.225 */
   GAR_ERR_INVALID_M = 3,        /* Multi-Krum m outside [1, n-f-2] (l.210)                              */
   GAR_ERR_ALIGNMENT = 4,        /* a row or out pointer not 16-byte aligned                             */
-  GAR_ERR_UNSUPPORTED = 5,      /* selection asked of a coordinate-wise rule                           */
+  GAR_ERR_UNSUPPORTED = 5,      /* selection asked of a coordinate-wise rule; MDA beyond its budget    */
   GAR_ERR_WORKSPACE = 6,        /* workspace missing or smaller than gar_workspace_bytes()             */
   GAR_ERR_CUDA = 7              /* a CUDA call or kernel launch failed                                  */
 } gar_status;
@@ -98,8 +100,9 @@ gar_status gar_aggregate_ex(gar_rule rule, const float* const* grads, int n, int
                             int64_t d, float* out, int32_t* indices_dev, void* workspace,
                             size_t workspace_bytes, gar_stream_t stream);
 
-/* Selection only (Krum, Multi-Krum, Bulyan): indices in selection order —
- * ascending (score, index) for Krum/Multi-Krum, round order for Bulyan — into
+/* Selection only (Krum, Multi-Krum, Bulyan, MDA): indices in selection order
+ * — ascending (score, index) for Krum/Multi-Krum, round order for Bulyan,
+ * ascending index for MDA's minimum-diameter subset of n - f — into
  * indices_dev.  *n_selected_host (optional) receives the count, known
  * without synchronising. */
 gar_status gar_select(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d,
@@ -125,14 +128,16 @@ gar_status gar_gram_partial(const float* const* grads, int n, int64_t d_local, d
                             void* workspace, size_t workspace_bytes, gar_stream_t stream);
 
 /* Selection from a (summed) Gram matrix; same outputs as gar_select.
- * workspace: >= gar_workspace_bytes(rule, n, f, 0) bytes. */
+ * workspace: >= gar_workspace_bytes(rule, n, f, 0) bytes (required for MDA,
+ * unused by the others). */
 gar_status gar_select_from_gram(gar_rule rule, const double* gram_dev, int n, int f, int m,
                                 int32_t* indices_dev, int* n_selected_host, void* workspace,
                                 size_t workspace_bytes, gar_stream_t stream);
 
 /* Combine step on a coordinate slice given the selection: Krum copies the
- * selected row, Multi-Krum averages the m selected rows, Bulyan runs its
- * coordinate phase over the n-2f selected rows.  indices_dev as produced by
+ * selected row, Multi-Krum averages the m selected rows, MDA the n-f selected
+ * rows (fp64, index order), Bulyan runs its coordinate phase over the n-2f
+ * selected rows.  indices_dev as produced by
  * gar_select / gar_select_from_gram. */
 gar_status gar_combine(gar_rule rule, const float* const* grads, int n, int f, int m,
                        int64_t d_local, const int32_t* indices_dev, float* out,

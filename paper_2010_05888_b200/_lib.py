@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libgar.so" if not os.environ.get("GAR_LIB_VARIAN
                         "libgar_" + os.environ["GAR_LIB_VARIANT"] + ".so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "gar.h")
 
-RULES = {"average": 0, "median": 1, "trimmed_mean": 2, "krum": 3, "multi_krum": 4, "bulyan": 5}
+RULES = {"average": 0, "median": 1, "trimmed_mean": 2, "krum": 3, "multi_krum": 4, "bulyan": 5, "mda": 6}
 STATUS = {0: "GAR_OK", 1: "GAR_ERR_INVALID_ARGUMENT", 2: "GAR_ERR_QUORUM", 3: "GAR_ERR_INVALID_M",
           4: "GAR_ERR_ALIGNMENT", 5: "GAR_ERR_UNSUPPORTED", 6: "GAR_ERR_WORKSPACE", 7: "GAR_ERR_CUDA"}
 MAX_N = 64
@@ -214,10 +214,12 @@ def gar_gram_partial(grads, gram: torch.Tensor, workspace: torch.Tensor, d: int 
 
 
 def gar_select_from_gram(rule, gram: torch.Tensor, n: int, f: int, m: int, indices: torch.Tensor,
-                         stream=None) -> int:
+                         stream=None, workspace: torch.Tensor | None = None) -> int:
+    """workspace: required for MDA (gar_workspace_bytes), unused otherwise."""
     nsel = ctypes.c_int(0)
+    wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
     check(lib.gar_select_from_gram(rule_id(rule), _ptr(gram), n, f, m, _ptr(indices), ctypes.byref(nsel),
-                                   None, 0, stream_handle(gram.device, stream)), "gar_select_from_gram")
+                                   _ptr(workspace), wsb, stream_handle(gram.device, stream)), "gar_select_from_gram")
     return nsel.value
 
 

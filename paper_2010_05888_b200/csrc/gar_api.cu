@@ -19,15 +19,30 @@ using gar::CoordLaunch;
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-bool is_krum_family(gar_rule r) { return r == GAR_KRUM || r == GAR_MULTI_KRUM || r == GAR_BULYAN; }
+// The selection rules: Gram matrix -> selected inputs -> combine.
+bool is_krum_family(gar_rule r) {
+  return r == GAR_KRUM || r == GAR_MULTI_KRUM || r == GAR_BULYAN || r == GAR_MDA;
+}
 
-bool valid_rule(int r) { return r >= GAR_AVERAGE && r <= GAR_BULYAN; }
+bool valid_rule(int r) { return r >= GAR_AVERAGE && r <= GAR_MDA; }
 
-// Effective m for (rule, n, f, m): Krum 1, Multi-Krum m (0 -> n-f-2).
+// Effective m for (rule, n, f, m): Krum 1, Multi-Krum m (0 -> n-f-2), MDA n-f.
 int effective_m(gar_rule rule, int n, int f, int m) {
   if (rule == GAR_KRUM) return 1;
   if (rule == GAR_MULTI_KRUM) return m == 0 ? n - f - 2 : m;
+  if (rule == GAR_MDA) return n - f;
   return 0;
+}
+
+// MDA enumerates the C(n, f) excluded sets: bounded (~2e9 subsets, seconds).
+constexpr uint64_t kMdaMaxSubsets = 1ull << 31;
+bool mda_within_budget(int n, int f) {
+  uint64_t c = 1;
+  for (int i = 1; i <= f; ++i) {
+    c = c * uint64_t(n - f + i) / uint64_t(i);
+    if (c > kMdaMaxSubsets) return false;
+  }
+  return true;
 }
 
 // Pure argument checks (no CUDA calls): rule, sizes, quorum (PAPER.md l.208,
@@ -46,6 +61,9 @@ gar_status check_rule_args(gar_rule rule, int n, int f, int m) {
       return GAR_OK;
     }
     case GAR_BULYAN: return n >= 4 * f + 3 ? GAR_OK : GAR_ERR_QUORUM;
+    case GAR_MDA:
+      if (n < 2 * f + 1) return GAR_ERR_QUORUM;
+      return mda_within_budget(n, f) ? GAR_OK : GAR_ERR_UNSUPPORTED;
   }
   return GAR_ERR_INVALID_ARGUMENT;
 }
@@ -150,12 +168,16 @@ struct Workspace {
   double* partials;
   double* G;
   int32_t* idx;
+  double* D;       // MDA: the distance matrix
+  void* mda;       // MDA: enumeration scratch
 };
 
 size_t ws_bytes_for(int n) {
   size_t b = align_up(sizeof(double) * gar::kGramMaxParts * n * n, 256);
   b += align_up(sizeof(double) * n * n, 256);
   b += align_up(sizeof(int32_t) * GAR_MAX_N, 256);
+  b += align_up(sizeof(double) * n * n, 256);
+  b += align_up(gar::mda_workspace_bytes(n), 256);
   return b;
 }
 
@@ -167,6 +189,10 @@ Workspace carve(void* ws, int n) {
   w.G = reinterpret_cast<double*>(p);
   p += align_up(sizeof(double) * n * n, 256);
   w.idx = reinterpret_cast<int32_t*>(p);
+  p += align_up(sizeof(int32_t) * GAR_MAX_N, 256);
+  w.D = reinterpret_cast<double*>(p);
+  p += align_up(sizeof(double) * n * n, 256);
+  w.mda = p;
   return w;
 }
 
@@ -178,7 +204,13 @@ gar_status run_gram(const float* const* grads, int n, int64_t d, const Workspace
 }
 
 gar_status run_select(gar_rule rule, const double* G, int n, int f, int me, int32_t* idx, double* D_out,
-                      cudaStream_t st) {
+                      const Workspace* w, cudaStream_t st) {
+  if (rule == GAR_MDA) {
+    if (!w) return GAR_ERR_WORKSPACE;
+    gar_status s = cuda_status(gar::launch_select(G, n, 0, 0, gar::kSelDistancesOnly, w->idx, w->D, st));
+    if (s != GAR_OK) return s;
+    return cuda_status(gar::launch_mda_select(w->D, n, f, w->mda, num_sms(), idx, st));
+  }
   const int srule = (rule == GAR_BULYAN) ? gar::kSelBulyan : gar::kSelMultiKrum;
   return cuda_status(gar::launch_select(G, n, f, me, srule, idx, D_out, st));
 }
@@ -259,7 +291,7 @@ gar_status aggregate_impl(gar_rule rule, const float* const* grads, int n, int f
   Workspace w = carve(workspace, n);
   int32_t* idx = indices_dev ? indices_dev : w.idx;
   if ((s = run_gram(grads, n, d, w, st)) != GAR_OK) return s;
-  if ((s = run_select(rule, w.G, n, f, me, idx, nullptr, st)) != GAR_OK) return s;
+  if ((s = run_select(rule, w.G, n, f, me, idx, nullptr, &w, st)) != GAR_OK) return s;
   return run_combine(rule, grads, n, f, me, d, idx, out, extra, st);
 }
 
@@ -305,7 +337,7 @@ size_t gar_workspace_bytes(gar_rule rule, int n, int f, int64_t d) {
 int gar_num_selected(gar_rule rule, int n, int f, int m) {
   if (check_rule_args(rule, n, f, m) != GAR_OK) return 0;
   if (rule == GAR_BULYAN) return n - 2 * f;
-  return effective_m(rule, n, f, m);
+  return effective_m(rule, n, f, m);   // Krum 1, Multi-Krum m, MDA n - f
 }
 
 gar_status gar_aggregate_ex(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d,
@@ -357,7 +389,7 @@ gar_status gar_select(gar_rule rule, const float* const* grads, int n, int f, in
   const int me = effective_m(rule, n, f, m);
   Workspace w = carve(workspace, n);
   if ((s = run_gram(grads, n, d, w, st)) != GAR_OK) return s;
-  if ((s = run_select(rule, w.G, n, f, me, indices_dev, nullptr, st)) != GAR_OK) return s;
+  if ((s = run_select(rule, w.G, n, f, me, indices_dev, nullptr, &w, st)) != GAR_OK) return s;
   if (n_selected_host) *n_selected_host = gar_num_selected(rule, n, f, m);
   return GAR_OK;
 }
@@ -395,17 +427,21 @@ gar_status gar_gram_partial(const float* const* grads, int n, int64_t d_local, d
 gar_status gar_select_from_gram(gar_rule rule, const double* gram_dev, int n, int f, int m, int32_t* indices_dev,
                                 int* n_selected_host, void* workspace, size_t workspace_bytes,
                                 gar_stream_t stream) {
-  (void)workspace;
-  (void)workspace_bytes;
   gar_status s = check_rule_args(rule, n, f, m);
   if (s != GAR_OK) return s;
   if (!is_krum_family(rule)) return GAR_ERR_UNSUPPORTED;
   if (!gram_dev || !indices_dev) return GAR_ERR_INVALID_ARGUMENT;
+  // MDA needs the workspace (distance matrix + enumeration scratch); the
+  // other rules run in one CTA's shared memory
+  if (rule == GAR_MDA && (!workspace || workspace_bytes < ws_bytes_for(n))) return GAR_ERR_WORKSPACE;
   if ((s = check_device_ptr(gram_dev)) != GAR_OK) return s;
   if ((s = check_device_ptr(indices_dev)) != GAR_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int me = effective_m(rule, n, f, m);
-  if ((s = run_select(rule, gram_dev, n, f, me, indices_dev, nullptr, st)) != GAR_OK) return s;
+  Workspace w{};
+  if (workspace) w = carve(workspace, n);
+  if ((s = run_select(rule, gram_dev, n, f, me, indices_dev, nullptr, workspace ? &w : nullptr, st)) != GAR_OK)
+    return s;
   if (n_selected_host) *n_selected_host = gar_num_selected(rule, n, f, m);
   return GAR_OK;
 }

@@ -47,6 +47,13 @@ cudaError_t launch_gram_exchange(const double* partials, int n_parts, int n, con
                                  const PeerFlags& flags, int world, int rank, uint32_t epoch, double* G,
                                  cudaStream_t stream);
 
+// MDA selection (mda.cu): scratch of mda_workspace_bytes(n) bytes, at most
+// kMdaMaxCtas enumeration CTAs; idx_out = the n - f kept indices, ascending.
+constexpr int kMdaMaxCtas = 1024;
+size_t mda_workspace_bytes(int n);
+cudaError_t launch_mda_select(const double* D, int n, int f, void* scratch, int num_sms, int32_t* idx_out,
+                              cudaStream_t stream);
+
 // Trimmed-set membership masks (membership.cu; verification entry point).
 cudaError_t launch_trimmed_membership(const float* const* rows, int n, int f, int64_t d, uint64_t* mask,
                                       int num_sms, cudaStream_t stream);

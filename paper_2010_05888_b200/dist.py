@@ -39,7 +39,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-KRUM_FAMILY = ("krum", "multi_krum", "bulyan")
+KRUM_FAMILY = ("krum", "multi_krum", "bulyan", "mda")     # the Gram-based selection rules
 
 
 def shard_bounds(d: int, rank: int, world: int, align: int = 1024) -> tuple[int, int]:
@@ -69,8 +69,8 @@ class _LibgarBackend:
     def gram_partial(self, rows, gram, ws, d):
         self._lib.gar_gram_partial(rows, gram, ws, d=d)
 
-    def select_from_gram(self, rule, gram, n, f, m, idx):
-        return self._lib.gar_select_from_gram(rule, gram, n, f, m, idx)
+    def select_from_gram(self, rule, gram, n, f, m, idx, ws=None):
+        return self._lib.gar_select_from_gram(rule, gram, n, f, m, idx, workspace=ws)
 
     def gram_exchange(self, rows, gram, ws, d, slots, flags, rank, world, epoch):
         self._lib.gar_gram_exchange(rows, gram, ws, slots, flags, rank, world, epoch, d=d)
@@ -246,7 +246,7 @@ class ShardedAggregator:
             out_local = torch.empty(self.d_local, dtype=torch.float32, device=dev)
         if self.rule in KRUM_FAMILY:
             self._gram_whole(rows_local, dev, mark)
-            self.backend.select_from_gram(self.rule, self._gram, self.n, self.f, self.m, self._idx)
+            self.backend.select_from_gram(self.rule, self._gram, self.n, self.f, self.m, self._idx, ws=self._ws)
             mark("select")
             self.backend.combine(self.rule, rows_local, self.f, self.m, self._idx, out_local, self.d_local)
             mark("combine")
@@ -289,7 +289,7 @@ class ShardedAggregator:
         out_local = buf[self.lo: self.hi]
         if self.rule in KRUM_FAMILY:
             self._gram_whole(rows_local, dev, mark)
-            self.backend.select_from_gram(self.rule, self._gram, self.n, self.f, self.m, self._idx)
+            self.backend.select_from_gram(self.rule, self._gram, self.n, self.f, self.m, self._idx, ws=self._ws)
             mark("select")
             self.backend.combine(self.rule, rows_local, self.f, self.m, self._idx, out_local, self.d_local, extra)
             mark("combine")

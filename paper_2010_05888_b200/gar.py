@@ -19,7 +19,7 @@ class Aggregator:
         self.n, self.f = int(n), int(f)
         self.m = 0 if m is None else int(m)
         # argument check (quorum, m) without touching the GPU
-        if rule in ("krum", "multi_krum", "bulyan"):
+        if rule in ("krum", "multi_krum", "bulyan", "mda"):
             if _lib.gar_num_selected(rule, self.n, self.f, self.m) == 0:
                 raise _lib.GarError(2 if self.m == 0 else 3, f"init({rule!r}, n={n}, f={f}, m={m})")
         elif _lib.gar_workspace_bytes(rule, self.n, self.f, 0) == 0 and not self._coord_ok():

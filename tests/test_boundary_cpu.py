@@ -113,7 +113,7 @@ def test_python_binding_validates_before_gpu():
     with pytest.raises(GarError):
         init("multi_krum", 10, 2, m=7)
     with pytest.raises(ValueError):
-        init("mda", 10, 2)
+        init("geometric_median", 10, 2)
     g = init("median", 5, 2)
     with pytest.raises(ValueError):          # CPU tensors are rejected: no CPU fallback
         g.aggregate([torch.zeros(8) for _ in range(5)])
@@ -174,3 +174,14 @@ def test_gram_exchange_checks_its_peer_arrays(gl):
     assert call([0x70_0000, 0], ok_f, 0, 2) == 1         # null slot array
     assert call([0x70_0004, 0x71_0000], ok_f, 0, 2) == 4  # misaligned slot array
     assert call(ok_s, ok_f, 1, 2) in (1, 7)             # valid: reaches the device check (no GPU here)
+
+
+def test_mda_arguments(gl):
+    """MDA: quorum n >= 2f+1, n - f selected, enumeration
+    budget C(n, f) <= 2^31 (GAR_ERR_UNSUPPORTED above)."""
+    assert gl.gar_num_selected("mda", 11, 2, 0) == 9
+    assert gl.gar_num_selected("mda", 4, 2, 0) == 0
+    assert gl.gar_workspace_bytes("mda", 31, 7, 100) > 0
+    assert _call_ex(gl, "mda", 4, 2, 0, 100, ws=0x30_0000, wsb=1 << 30) == 2
+    assert _call_ex(gl, "mda", 64, 30, 0, 100, ws=0x30_0000, wsb=1 << 30) == 5
+    assert _call_ex(gl, "mda", 31, 7, 0, 100, ws=0x30_0000, wsb=1 << 30) in (1, 7)

@@ -32,7 +32,7 @@ class HostBackend:
         x = rows[:, :d].numpy().astype(np.float64)
         gram.copy_(torch.from_numpy(x @ x.T))
 
-    def select_from_gram(self, rule, gram, n, f, m, idx):
+    def select_from_gram(self, rule, gram, n, f, m, idx, ws=None):
         import oracle
         G = gram.numpy()
         g = np.diag(G)

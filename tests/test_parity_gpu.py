@@ -186,6 +186,47 @@ def test_fused_server_step(gar, n, f, d):
             assert_same_bits(params2.cpu().numpy(), expect, f"{rule} fused combine step")
 
 
+@pytest.mark.parametrize("n,f,d", [(1, 0, 100), (3, 1, 1000), (7, 2, 4099), (11, 2, 79_510), (15, 3, 20_003),
+                                   (31, 7, 50_000), (64, 2, 3000)])
+def test_mda_parity(gar, n, f, d):
+    """MDA: the GPU's minimum-diameter subset equals the
+    oracle's, or its diameter (oracle distances) is within 1e-5 of the
+    minimum (eps-tie); the output equals the oracle's average of the GPU's
+    subset bit for bit."""
+    x = synth.make_gradients(n, f, d, seed=synth.BASE_SEED + 31 + n, ld=d).numpy() if n >= 3 else \
+        np.random.default_rng(n).standard_normal((n, d)).astype(np.float32)
+    X = to_device(x)
+    a = gar.init("mda", n, f)
+    out = a.aggregate(X, out=torch.empty(d, dtype=torch.float32, device="cuda"), d=d)
+    sel = a.select(X, d=d).cpu().numpy()
+    torch.cuda.synchronize()
+    ref_out, ref_sel, D = oracle.mda(x, f, return_D=True)
+    assert len(sel) == n - f and list(sel) == sorted(sel)
+
+    def diam(s):
+        return max((D[i, j] for i in s for j in s if i < j), default=0.0)
+    if list(sel) != list(ref_sel):
+        assert diam(sel) <= diam(ref_sel) * (1 + 1e-5), (sel, ref_sel, diam(sel), diam(ref_sel))
+    assert_same_bits(out.cpu().numpy(), oracle.mean_of_rows(x, sel), "mda output")
+
+
+def test_mda_special_inputs(gar):
+    """SPEC S:89-91 ([(0), (1), (100)], f = 1 -> 0.5); identical inputs -> the
+    lexicographically first subset and the input itself."""
+    x = np.array([[0.0], [1.0], [100.0]], np.float32)
+    out = gar.init("mda", 3, 1).aggregate(to_device(x), d=1)
+    torch.cuda.synchronize()
+    assert out.cpu().numpy()[0] == np.float32(0.5)
+    v = np.random.default_rng(2).standard_normal(777).astype(np.float32)
+    xs = np.tile(v, (9, 1))
+    a = gar.init("mda", 9, 3)
+    out = a.aggregate(to_device(xs), d=777)
+    sel = a.select(to_device(xs), d=777).cpu().numpy()
+    torch.cuda.synchronize()
+    assert list(sel) == list(range(6))
+    assert_same_bits(out.cpu().numpy(), v, "mda identical")
+
+
 def test_graphed_aggregate_matches_eager(gar):
     """Aggregator.graphed: a CUDA graph of the call, replayed on new contents
     of the same buffers, equals the eager call bit for bit."""
