@@ -149,6 +149,32 @@ def _ptr(t):
     return ctypes.c_void_p(0 if t is None else t.data_ptr())
 
 
+def _idx(indices, rule, n, f, m, dev, optional):
+    """Selected-index buffer: int32 on `dev`, room for gar_num_selected."""
+    return _buf(indices, torch.int32, max(1, gar_num_selected(rule, n, f, m)), dev, "indices", optional)
+
+
+def _buf(t, dtype, numel: int, dev, what: str, optional: bool = False):
+    """Pointer to a caller buffer after the checks the C ABI cannot make:
+    a contiguous CUDA tensor of `dtype` on the gradients' device holding at
+    least `numel` elements (None allowed when optional)."""
+    if t is None:
+        if optional:
+            return ctypes.c_void_p(0)
+        raise ValueError(f"{what} is required")
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{what} must be a torch.Tensor")
+    if t.device.type != "cuda" or (dev is not None and t.device != dev):
+        raise ValueError(f"{what} must live on the gradients' CUDA device ({dev}), not {t.device}")
+    if t.dtype not in ((dtype,) if not isinstance(dtype, tuple) else dtype):
+        raise TypeError(f"{what} must be {dtype}, not {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    if t.numel() < numel:
+        raise ValueError(f"{what} holds {t.numel()} elements, needs {numel}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
 def check(code: int, what: str):
     if code != 0:
         detail = lib.gar_last_error().decode() if code == 7 else ""
@@ -172,9 +198,17 @@ def gar_num_selected(rule, n: int, f: int, m: int = 0) -> int:
     return int(lib.gar_num_selected(rule_id(rule), n, f, m))
 
 
+def _wsb(workspace) -> int:
+    return 0 if workspace is None else workspace.numel() * workspace.element_size()
+
+
+def _f32(t, d, dev, what="out"):
+    return _buf(t, torch.float32, d, dev, what)
+
+
 def gar_aggregate(rule, grads, f: int, out: torch.Tensor, d: int | None = None, stream=None):
     arr, n, d, dev = row_pointers(grads, d)
-    check(lib.gar_aggregate(rule_id(rule), arr, n, f, d, _ptr(out), stream_handle(dev, stream)),
+    check(lib.gar_aggregate(rule_id(rule), arr, n, f, d, _f32(out, d, dev), stream_handle(dev, stream)),
           "gar_aggregate")
     return out
 
@@ -182,9 +216,9 @@ def gar_aggregate(rule, grads, f: int, out: torch.Tensor, d: int | None = None, 
 def gar_aggregate_ex(rule, grads, f: int, m: int, out: torch.Tensor, indices=None, workspace=None,
                      d: int | None = None, stream=None):
     arr, n, d, dev = row_pointers(grads, d)
-    wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    check(lib.gar_aggregate_ex(rule_id(rule), arr, n, f, m, d, _ptr(out), _ptr(indices), _ptr(workspace),
-                               wsb, stream_handle(dev, stream)), "gar_aggregate_ex")
+    o, ix = _f32(out, d, dev), _idx(indices, rule, n, f, m, dev, True)
+    check(lib.gar_aggregate_ex(rule_id(rule), arr, n, f, m, d, o, ix, _ptr(workspace), _wsb(workspace),
+                               stream_handle(dev, stream)), "gar_aggregate_ex")
     return out
 
 
@@ -192,23 +226,24 @@ def gar_select(rule, grads, f: int, m: int, indices: torch.Tensor, workspace: to
                d: int | None = None, stream=None) -> int:
     arr, n, d, dev = row_pointers(grads, d)
     nsel = ctypes.c_int(0)
-    check(lib.gar_select(rule_id(rule), arr, n, f, m, d, _ptr(indices), ctypes.byref(nsel), _ptr(workspace),
-                         workspace.numel() * workspace.element_size(), stream_handle(dev, stream)),
-          "gar_select")
+    ix = _idx(indices, rule, n, f, m, dev, False)
+    check(lib.gar_select(rule_id(rule), arr, n, f, m, d, ix, ctypes.byref(nsel), _ptr(workspace), _wsb(workspace),
+                         stream_handle(dev, stream)), "gar_select")
     return nsel.value
 
 
 def gar_distances(grads, D: torch.Tensor, workspace: torch.Tensor, d: int | None = None, stream=None):
     arr, n, d, dev = row_pointers(grads, d)
-    check(lib.gar_distances(arr, n, d, _ptr(D), _ptr(workspace), workspace.numel() * workspace.element_size(),
-                            stream_handle(dev, stream)), "gar_distances")
+    dp = _buf(D, torch.float64, n * n, dev, "D")
+    check(lib.gar_distances(arr, n, d, dp, _ptr(workspace), _wsb(workspace), stream_handle(dev, stream)),
+          "gar_distances")
     return D
 
 
 def gar_gram_partial(grads, gram: torch.Tensor, workspace: torch.Tensor, d: int | None = None, stream=None):
     arr, n, d, dev = row_pointers(grads, d)
-    check(lib.gar_gram_partial(arr, n, d, _ptr(gram), _ptr(workspace),
-                               workspace.numel() * workspace.element_size(), stream_handle(dev, stream)),
+    g = _buf(gram, torch.float64, n * n, dev, "gram")
+    check(lib.gar_gram_partial(arr, n, d, g, _ptr(workspace), _wsb(workspace), stream_handle(dev, stream)),
           "gar_gram_partial")
     return gram
 
@@ -217,17 +252,18 @@ def gar_select_from_gram(rule, gram: torch.Tensor, n: int, f: int, m: int, indic
                          stream=None, workspace: torch.Tensor | None = None) -> int:
     """workspace: required for MDA (gar_workspace_bytes), unused otherwise."""
     nsel = ctypes.c_int(0)
-    wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    check(lib.gar_select_from_gram(rule_id(rule), _ptr(gram), n, f, m, _ptr(indices), ctypes.byref(nsel),
-                                   _ptr(workspace), wsb, stream_handle(gram.device, stream)), "gar_select_from_gram")
+    dev = gram.device
+    g, ix = _buf(gram, torch.float64, n * n, dev, "gram"), _idx(indices, rule, n, f, m, dev, False)
+    check(lib.gar_select_from_gram(rule_id(rule), g, n, f, m, ix, ctypes.byref(nsel), _ptr(workspace),
+                                   _wsb(workspace), stream_handle(dev, stream)), "gar_select_from_gram")
     return nsel.value
 
 
 def gar_combine(rule, grads, f: int, m: int, indices: torch.Tensor, out: torch.Tensor, d: int | None = None,
                 stream=None):
     arr, n, d, dev = row_pointers(grads, d)
-    check(lib.gar_combine(rule_id(rule), arr, n, f, m, d, _ptr(indices), _ptr(out),
-                          stream_handle(dev, stream)), "gar_combine")
+    ix, o = _idx(indices, rule, n, f, m, dev, False), _f32(out, d, dev)
+    check(lib.gar_combine(rule_id(rule), arr, n, f, m, d, ix, o, stream_handle(dev, stream)), "gar_combine")
     return out
 
 
@@ -242,9 +278,9 @@ def gar_aggregate_bcast(rule, grads, f: int, m: int, out: torch.Tensor, extra_pt
     (ints: peer-mapped buffers, e.g. torch symmetric memory)."""
     arr, n, d, dev = row_pointers(grads, d)
     ex, ne = _ptr_array(extra_ptrs)
-    wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    check(lib.gar_aggregate_bcast(rule_id(rule), arr, n, f, m, d, _ptr(out), ex, ne, _ptr(indices), _ptr(workspace),
-                                  wsb, stream_handle(dev, stream)), "gar_aggregate_bcast")
+    o, ix = _f32(out, d, dev), _idx(indices, rule, n, f, m, dev, True)
+    check(lib.gar_aggregate_bcast(rule_id(rule), arr, n, f, m, d, o, ex, ne, ix, _ptr(workspace), _wsb(workspace),
+                                  stream_handle(dev, stream)), "gar_aggregate_bcast")
     return out
 
 
@@ -252,8 +288,9 @@ def gar_combine_bcast(rule, grads, f: int, m: int, indices: torch.Tensor, out: t
                       d: int | None = None, stream=None):
     arr, n, d, dev = row_pointers(grads, d)
     ex, ne = _ptr_array(extra_ptrs)
-    check(lib.gar_combine_bcast(rule_id(rule), arr, n, f, m, d, _ptr(indices), _ptr(out), ex, ne,
-                                stream_handle(dev, stream)), "gar_combine_bcast")
+    ix, o = _idx(indices, rule, n, f, m, dev, False), _f32(out, d, dev)
+    check(lib.gar_combine_bcast(rule_id(rule), arr, n, f, m, d, ix, o, ex, ne, stream_handle(dev, stream)),
+          "gar_combine_bcast")
     return out
 
 
@@ -262,16 +299,17 @@ def gar_aggregate_mcast(rule, grads, f: int, m: int, out: torch.Tensor, out_mc: 
     """gar_aggregate_ex with the result stored through the multicast address
     out_mc (an int) that maps `out` on every member GPU."""
     arr, n, d, dev = row_pointers(grads, d)
-    wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    check(lib.gar_aggregate_mcast(rule_id(rule), arr, n, f, m, d, _ptr(out), ctypes.c_void_p(out_mc), _ptr(indices),
-                                  _ptr(workspace), wsb, stream_handle(dev, stream)), "gar_aggregate_mcast")
+    o, ix = _f32(out, d, dev), _idx(indices, rule, n, f, m, dev, True)
+    check(lib.gar_aggregate_mcast(rule_id(rule), arr, n, f, m, d, o, ctypes.c_void_p(out_mc), ix, _ptr(workspace),
+                                  _wsb(workspace), stream_handle(dev, stream)), "gar_aggregate_mcast")
     return out
 
 
 def gar_combine_mcast(rule, grads, f: int, m: int, indices: torch.Tensor, out: torch.Tensor, out_mc: int,
                       d: int | None = None, stream=None):
     arr, n, d, dev = row_pointers(grads, d)
-    check(lib.gar_combine_mcast(rule_id(rule), arr, n, f, m, d, _ptr(indices), _ptr(out), ctypes.c_void_p(out_mc),
+    ix, o = _idx(indices, rule, n, f, m, dev, False), _f32(out, d, dev)
+    check(lib.gar_combine_mcast(rule_id(rule), arr, n, f, m, d, ix, o, ctypes.c_void_p(out_mc),
                                 stream_handle(dev, stream)), "gar_combine_mcast")
     return out
 
@@ -280,8 +318,8 @@ def gar_trimmed_membership(grads, f: int, mask: torch.Tensor, d: int | None = No
     """mask: device int64[d] (uint64 bit patterns): bit i set iff input i is kept
     by the trimmed mean at that coordinate."""
     arr, n, d, dev = row_pointers(grads, d)
-    check(lib.gar_trimmed_membership(arr, n, f, d, _ptr(mask), stream_handle(dev, stream)),
-          "gar_trimmed_membership")
+    mk = _buf(mask, (torch.int64, torch.uint64), d, dev, "mask")
+    check(lib.gar_trimmed_membership(arr, n, f, d, mk, stream_handle(dev, stream)), "gar_trimmed_membership")
     return mask
 
 
@@ -292,9 +330,9 @@ def gar_gram_exchange(grads, gram: torch.Tensor, workspace: torch.Tensor, peer_s
     arr, n, d, dev = row_pointers(grads, d)
     sl, _ = _ptr_array(peer_slots)
     fl, _ = _ptr_array(peer_flags)
-    check(lib.gar_gram_exchange(arr, n, d, sl, fl, rank, world, epoch, _ptr(gram), _ptr(workspace),
-                                workspace.numel() * workspace.element_size(), stream_handle(dev, stream)),
-          "gar_gram_exchange")
+    g = _buf(gram, torch.float64, n * n, dev, "gram")
+    check(lib.gar_gram_exchange(arr, n, d, sl, fl, rank, world, epoch, g, _ptr(workspace), _wsb(workspace),
+                                stream_handle(dev, stream)), "gar_gram_exchange")
     return gram
 
 
@@ -302,15 +340,16 @@ def gar_aggregate_sgd(rule, grads, f: int, m: int, params: torch.Tensor, lr: flo
                       d: int | None = None, stream=None):
     """params <- params - lr * GAR(grads), fused into the producing kernel."""
     arr, n, d, dev = row_pointers(grads, d)
-    wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    check(lib.gar_aggregate_sgd(rule_id(rule), arr, n, f, m, d, _ptr(params), float(lr), _ptr(indices),
-                                _ptr(workspace), wsb, stream_handle(dev, stream)), "gar_aggregate_sgd")
+    pp, ix = _f32(params, d, dev, "params"), _idx(indices, rule, n, f, m, dev, True)
+    check(lib.gar_aggregate_sgd(rule_id(rule), arr, n, f, m, d, pp, float(lr), ix, _ptr(workspace), _wsb(workspace),
+                                stream_handle(dev, stream)), "gar_aggregate_sgd")
     return params
 
 
 def gar_combine_sgd(rule, grads, f: int, m: int, indices: torch.Tensor, params: torch.Tensor, lr: float,
                     d: int | None = None, stream=None):
     arr, n, d, dev = row_pointers(grads, d)
-    check(lib.gar_combine_sgd(rule_id(rule), arr, n, f, m, d, _ptr(indices), _ptr(params), float(lr),
-                              stream_handle(dev, stream)), "gar_combine_sgd")
+    ix, pp = _idx(indices, rule, n, f, m, dev, False), _f32(params, d, dev, "params")
+    check(lib.gar_combine_sgd(rule_id(rule), arr, n, f, m, d, ix, pp, float(lr), stream_handle(dev, stream)),
+          "gar_combine_sgd")
     return params

@@ -71,8 +71,9 @@ class Aggregator:
             out = torch.empty(d, dtype=torch.float32, device=dev)
         ws = self.workspace(dev)
         wsb = 0 if ws is None else ws.numel()
-        _lib.check(_lib.lib.gar_aggregate_ex(self.rid, arr, n, self.f, self.m, d, _lib._ptr(out),
-                                             _lib._ptr(indices), _lib._ptr(ws), wsb,
+        o = _lib._buf(out, torch.float32, d, dev, "out")
+        ix = _lib._idx(indices, self.rule, n, self.f, self.m, dev, True)
+        _lib.check(_lib.lib.gar_aggregate_ex(self.rid, arr, n, self.f, self.m, d, o, ix, _lib._ptr(ws), wsb,
                                              _lib.stream_handle(dev, stream)), f"aggregate[{self.rule}]")
         return out
 
