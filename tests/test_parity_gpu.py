@@ -227,6 +227,25 @@ def test_mda_special_inputs(gar):
     assert_same_bits(out.cpu().numpy(), v, "mda identical")
 
 
+def test_binding_rejects_bad_buffers(gar):
+    """The binding checks what the C ABI cannot: dtype, device, size."""
+    n, f, d = 7, 1, 1000
+    X = torch.zeros((n, d), dtype=torch.float32, device="cuda")
+    a = gar.init("median", n, f)
+    with pytest.raises(TypeError):
+        a.aggregate(X, out=torch.empty(d, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        a.aggregate(X, out=torch.empty(d - 1, dtype=torch.float32, device="cuda"))
+    with pytest.raises(ValueError):
+        a.aggregate(X, out=torch.empty(d, dtype=torch.float32))
+    k = gar.init("multi_krum", n, f)
+    ws = k.workspace(torch.device("cuda"))
+    with pytest.raises(ValueError):          # room for fewer than m = n - f - 2 indices
+        gar.gar_select("multi_krum", X, f, 0, torch.empty(2, dtype=torch.int32, device="cuda"), ws, d=d)
+    with pytest.raises(ValueError):
+        gar.gar_gram_partial(X, torch.empty(n * n - 1, dtype=torch.float64, device="cuda"), ws, d=d)
+
+
 def test_graphed_aggregate_matches_eager(gar):
     """Aggregator.graphed: a CUDA graph of the call, replayed on new contents
     of the same buffers, equals the eager call bit for bit."""
