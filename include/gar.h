@@ -54,14 +54,16 @@ typedef enum {
   GAR_KRUM = 3,         /* Multi-Krum with m = 1, l.210-212; R10                     */
   GAR_MULTI_KRUM = 4,   /* average of the m smallest-score inputs, l.210-212         */
   GAR_BULYAN = 5,       /* iterated Krum + coordinate phase, l.219-225; R7, R8       */
-  GAR_MDA = 6           /* minimum-diameter averaging, l.214-217; R13; q >= 2f+1,   */
+  GAR_MDA = 6,          /* minimum-diameter averaging, l.214-217; R13; q >= 2f+1,   */
                         /* C(q, f) <= 2^31 (GAR_ERR_UNSUPPORTED above)              */
+  GAR_MEAN_AROUND_MEDIAN = 7 /* per coordinate, mean of the n-2f values closest to   */
+                        /* the median, l.316 fn.; R14; q >= 2f+1                    */
 } gar_rule;
 
 typedef enum {
   GAR_OK = 0,
   GAR_ERR_INVALID_ARGUMENT = 1, /* null/host pointer, n outside [1,64], f<0, d<0, out aliases an input, bad rule */
-  GAR_ERR_QUORUM = 2,           /* n < 2f+1 (median, trimmed, MDA) | 2f+3 (Krum family) | 4f+3 (Bulyan); l.208, l.212, l.217, l.225 */
+  GAR_ERR_QUORUM = 2,           /* n < 2f+1 (median, trimmed, MDA, mean around median) | 2f+3 (Krum family) | 4f+3 (Bulyan); l.208, l.212, l.217, l.225 */
   GAR_ERR_INVALID_M = 3,        /* Multi-Krum m outside [1, n-f-2] (l.210)                              */
   GAR_ERR_ALIGNMENT = 4,        /* a row or out pointer not 16-byte aligned                             */
   GAR_ERR_UNSUPPORTED = 5,      /* selection asked of a coordinate-wise rule; MDA beyond its budget    */

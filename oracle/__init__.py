@@ -69,6 +69,7 @@ def lib():
             "oracle_multi_krum": [f32p, I, I, I, L64, f32p, i32p, f64p, I],
             "oracle_bulyan": [f32p, I, I, L64, f32p, i32p, f64p, I],
             "oracle_mda_select": [f64p, I, I, i32p],
+            "oracle_mean_around_median": [f32p, I, I, L64, f32p, I],
             "oracle_mda": [f32p, I, I, L64, f32p, i32p, f64p, I],
         }
         for name, args in sig.items():
@@ -234,6 +235,17 @@ def multi_krum(x, f, m=None, threads=None, return_D=False):
                                    _p(sel, ctypes.c_int32), _p(D, ctypes.c_double),
                                    threads or default_threads()), "multi_krum")
     return (out, sel, D) if return_D else (out, sel)
+
+
+def mean_around_median(x, f, threads=None):
+    """Per coordinate, the mean of the n - 2f values closest to the median
+    (Bulyan's coordinate phase over all n inputs; PAPER.md l.316 footnote)."""
+    x = _f32(x)
+    n, d = x.shape
+    out = np.empty(d, np.float32)
+    _check(lib().oracle_mean_around_median(_p(x, ctypes.c_float), n, f, d, _p(out, ctypes.c_float),
+                                           threads or default_threads()), "mean_around_median")
+    return out
 
 
 def mda_select(D, f):

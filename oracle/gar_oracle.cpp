@@ -424,6 +424,19 @@ int oracle_mda_select(const double* D, int n, int f, int32_t* sel) {
   return 0;
 }
 
+// ---- Mean around median (PAPER.md l.316 footnote, "other Median-based
+// aggregation techniques ... mean around median"): per
+// coordinate, the n - 2f values closest to the coordinate-wise median,
+// averaged -- Bulyan's coordinate phase (R8) applied to all n inputs
+// (reading R14).  Requires n >= 2f + 1.
+int oracle_mean_around_median(const float* x, int n, int f, int64_t d, float* out, int threads) {
+  if (!x || !out || n < 1 || f < 0 || d < 0) return 1;
+  if (n < 2 * f + 1) return 2;
+  std::vector<int32_t> all(n);
+  for (int i = 0; i < n; ++i) all[i] = i;
+  return oracle_bulyan_coordinate_phase(x, n, f, d, all.data(), n, out, threads);
+}
+
 int oracle_mda(const float* x, int n, int f, int64_t d, float* out, int32_t* sel, double* D_out, int threads) {
   if (!x || !out || !sel || n < 1 || f < 0 || d < 0) return 1;
   if (n < 2 * f + 1) return 2;

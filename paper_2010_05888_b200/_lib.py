@@ -19,7 +19,8 @@ LIB_PATH = os.path.join(_HERE, "libgar.so" if not os.environ.get("GAR_LIB_VARIAN
                         "libgar_" + os.environ["GAR_LIB_VARIANT"] + ".so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "gar.h")
 
-RULES = {"average": 0, "median": 1, "trimmed_mean": 2, "krum": 3, "multi_krum": 4, "bulyan": 5, "mda": 6}
+RULES = {"average": 0, "median": 1, "trimmed_mean": 2, "krum": 3, "multi_krum": 4, "bulyan": 5, "mda": 6,
+         "mean_around_median": 7}
 STATUS = {0: "GAR_OK", 1: "GAR_ERR_INVALID_ARGUMENT", 2: "GAR_ERR_QUORUM", 3: "GAR_ERR_INVALID_M",
           4: "GAR_ERR_ALIGNMENT", 5: "GAR_ERR_UNSUPPORTED", 6: "GAR_ERR_WORKSPACE", 7: "GAR_ERR_CUDA"}
 MAX_N = 64

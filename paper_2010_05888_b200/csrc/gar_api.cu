@@ -24,7 +24,7 @@ bool is_krum_family(gar_rule r) {
   return r == GAR_KRUM || r == GAR_MULTI_KRUM || r == GAR_BULYAN || r == GAR_MDA;
 }
 
-bool valid_rule(int r) { return r >= GAR_AVERAGE && r <= GAR_MDA; }
+bool valid_rule(int r) { return r >= GAR_AVERAGE && r <= GAR_MEAN_AROUND_MEDIAN; }
 
 // Effective m for (rule, n, f, m): Krum 1, Multi-Krum m (0 -> n-f-2), MDA n-f.
 int effective_m(gar_rule rule, int n, int f, int m) {
@@ -52,7 +52,8 @@ gar_status check_rule_args(gar_rule rule, int n, int f, int m) {
   switch (rule) {
     case GAR_AVERAGE: return GAR_OK;
     case GAR_MEDIAN:
-    case GAR_TRIMMED_MEAN: return n >= 2 * f + 1 ? GAR_OK : GAR_ERR_QUORUM;
+    case GAR_TRIMMED_MEAN:
+    case GAR_MEAN_AROUND_MEDIAN: return n >= 2 * f + 1 ? GAR_OK : GAR_ERR_QUORUM;
     case GAR_KRUM:
     case GAR_MULTI_KRUM: {
       if (n < 2 * f + 3) return GAR_ERR_QUORUM;
@@ -285,6 +286,8 @@ gar_status aggregate_impl(gar_rule rule, const float* const* grads, int n, int f
     int mode = gar::kModeAverage;
     if (rule == GAR_MEDIAN) mode = gar::kModeMedian;
     if (rule == GAR_TRIMMED_MEAN) mode = gar::kModeTrimmed;
+    // mean around median = Bulyan's coordinate phase over all n inputs (R14)
+    if (rule == GAR_MEAN_AROUND_MEDIAN) mode = gar::kModeBulyan;
     return cuda_status(gar::launch_coord_select(mode, L, st));
   }
   const int me = effective_m(rule, n, f, m);

@@ -30,7 +30,7 @@ class Aggregator:
     def _coord_ok(self):
         if self.n < 1 or self.n > _lib.MAX_N or self.f < 0:
             return False
-        if self.rule in ("median", "trimmed_mean"):
+        if self.rule in ("median", "trimmed_mean", "mean_around_median"):
             return self.n >= 2 * self.f + 1
         return True
 

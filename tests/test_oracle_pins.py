@@ -452,3 +452,26 @@ def test_mda_special_cases_and_bounds():
         # permutation invariance (no diameter ties with continuous inputs)
         out2, _ = oracle.mda(xs[rng.permutation(n)], f)
         np.testing.assert_allclose(out2, out, rtol=1e-6, atol=1e-7)
+
+
+def test_mean_around_median_pins():
+    """PAPER.md l.316 footnote: f = 0 keeps everyone (Average on finite data);
+    n = 2f + 1 keeps only the median; range confinement with f planted
+    outliers; a brute force (sort by closeness to the median, ties by index)."""
+    rng = np.random.default_rng(31)
+    x = rng.standard_normal((9, 300)).astype(np.float32)
+    np.testing.assert_array_equal(oracle.mean_around_median(x, 0), oracle.average(x))   # exact fp64 sums
+    np.testing.assert_array_equal(oracle.mean_around_median(x, 4), oracle.median(x, 4))
+    h = (rng.standard_normal((8, 200)) * 0.1).astype(np.float32)
+    xs = np.concatenate([h, 1e6 * np.ones((3, 200), np.float32)])
+    out = oracle.mean_around_median(xs, 3)
+    assert np.all(out >= h.min(axis=0)) and np.all(out <= h.max(axis=0))
+    for k in range(0, 300, 37):
+        col = x[:, k].astype(np.float64)
+        med = np.median(col)
+        order = sorted(range(9), key=lambda i: (abs(np.float32(col[i]) - np.float32(med)), i))[:9 - 2 * 2]
+        kept = sorted(col[order])
+        s = 0.0
+        for v in kept:
+            s += v
+        assert np.float32(s / len(kept)) == oracle.mean_around_median(x, 2)[k]

@@ -227,6 +227,20 @@ def test_mda_special_inputs(gar):
     assert_same_bits(out.cpu().numpy(), v, "mda identical")
 
 
+@pytest.mark.parametrize("n,f", [(1, 0), (4, 1), (7, 2), (11, 2), (12, 3), (31, 7), (31, 15), (64, 15)])
+def test_mean_around_median_parity(gar, n, f):
+    """Mean around median (PAPER.md l.316 footnote, R14) bit-exact against the
+    oracle on recipe, tie-heavy and adversarial columns."""
+    rng = np.random.default_rng(500 + n + f)
+    d = 3 * 1031 + 1
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    x[:, :400] = rng.integers(-2, 3, (n, 400)).astype(np.float32)
+    x[:, -517:] = synth.adversarial_rows(n, 517, seed=n + f)
+    out = gar.init("mean_around_median", n, f).aggregate(to_device(x), d=d)
+    torch.cuda.synchronize()
+    assert_same_bits(out.cpu().numpy(), oracle.mean_around_median(x, f), "mean around median")
+
+
 def test_binding_rejects_bad_buffers(gar):
     """The binding checks what the C ABI cannot: dtype, device, size."""
     n, f, d = 7, 1, 1000
