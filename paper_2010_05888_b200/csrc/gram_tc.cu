@@ -41,20 +41,20 @@ namespace {
 
 template <int NP_>
 struct Cfg {
-  static constexpr int NP = NP_;                 // padded row count (16, 32 or 64)
+  static constexpr int NP = NP_;                 // padded row count (8, 16, 32 or 64)
   // Block-diagonal packing: a tile's coordinates are split into BLOCKS blocks
   // that share the MMA's K index; A = [H_0..H_{B-1}; L_0..L_{B-1}] and
   // B = [H_0..H_{B-1}], so the diagonal blocks of D = A B^T are the useful
   // H_b H_b^T and L_b H_b^T (off-diagonal blocks pair different coordinates
   // and are ignored).  NP = 32 -> 2 blocks, M = 128, N = 64: half the MMA
   // instructions of M = 64, N = 32 and the full 128-lane datapath.
-  static constexpr int BLOCKS = 64 / NP;         // 4 / 2 / 1
+  static constexpr int BLOCKS = 64 / NP;         // 8 / 4 / 2 / 1
   static constexpr int M = 2 * NP * BLOCKS;      // 128: H rows of all blocks, then L rows
   static constexpr int N = NP * BLOCKS;          // 64: H rows of all blocks
   static constexpr int CONV_WARPS = (NP <= 32) ? 8 : 4;   // converters: 16*CH coordinates each
-  static constexpr int CH = (NP == 16) ? 2 : 1;  // float4 chunks per lane per tile (per-tile costs vs rows)
-  static constexpr int KT = 16 * CH * CONV_WARPS;     // coordinates per tile: 256 / 128 / 64
-  static constexpr int KB = KT / BLOCKS;         // coordinates per block (MMA K extent): 64 / 64 / 64
+  static constexpr int CH = (NP == 8) ? 4 : (NP == 16) ? 2 : 1;  // float4 chunks per lane per tile
+  static constexpr int KT = 16 * CH * CONV_WARPS;     // coordinates per tile: 512 / 256 / 128 / 64
+  static constexpr int KB = KT / BLOCKS;         // coordinates per block (MMA K extent): 64 in every case
   static constexpr int ATOMS = KB / 32;          // 128-byte K atoms per tile
   static constexpr int ATOM_BYTES = M * 128;     // one K atom of A (8-row groups of 1 KB)
   static constexpr int OP_BYTES = ATOMS * ATOM_BYTES;      // one operand stage (A; B aliases its H rows)
@@ -64,11 +64,11 @@ struct Cfg {
   // each): bulk-copy issue is limited per request and per issuing warp
   // (tools/membench.cu, membench2.cu).
   static constexpr int PROD_WARPS = 3;     // 5 or 7 for NP = 64 measured slower (tools/gram_exp.sh)
-  static constexpr int RAW_SUB = (NP == 16) ? 2 : (NP == 32) ? 3 : 4;   // 2 KB / 1.5 KB / 1 KB per row
+  static constexpr int RAW_SUB = (NP == 8) ? 1 : (NP == 16) ? 2 : (NP == 32) ? 3 : 4;   // 2 / 2 / 1.5 / 1 KB per row
   static constexpr int RAW_KT = RAW_SUB * KT;    // coordinates per raw stage
   static constexpr int RAW_PITCH = RAW_KT * 4 + 16;   // bytes per raw row (+16: conflict-free LDS.128)
   static constexpr int RAW_BYTES = NP * RAW_PITCH;    // one raw stage (TMA destination)
-  static constexpr int RAW_STAGES = (NP == 16) ? 4 : (NP == 32) ? 3 : 2;
+  static constexpr int RAW_STAGES = (NP == 8) ? 8 : (NP == 16) ? 4 : (NP == 32) ? 3 : 2;
   // warp roles: converters | producers | epilogue | MMA = 16 warps (128 registers).
   static constexpr int PRODUCER_WARP = CONV_WARPS;
   static constexpr int EPI_WARP0 = CONV_WARPS + PROD_WARPS;
@@ -561,6 +561,7 @@ cudaError_t launch_gram_partials(const float* const* rows, int n, int64_t d, dou
                                  int* n_parts, cudaStream_t stream) {
   RowPtrs rp;
   for (int i = 0; i < GAR_MAX_N; ++i) rp.p[i] = (i < n) ? rows[i] : nullptr;
+  if (n <= 8) return launch_np<8>(rp, n, d, partials, num_sms, n_parts, stream);
   if (n <= 16) return launch_np<16>(rp, n, d, partials, num_sms, n_parts, stream);
   if (n <= 32) return launch_np<32>(rp, n, d, partials, num_sms, n_parts, stream);
   return launch_np<64>(rp, n, d, partials, num_sms, n_parts, stream);
