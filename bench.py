@@ -314,6 +314,11 @@ def run_ours(args):
         kernels[c] = {"ms_per_step": round(t, 4), "launches_per_step": launches[c],
                       "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 4),
                       "share_of_step": round(t / ms_step, 4)}
+    # libgar kernels per step: 1 per coordinate-wise rule; per Krum-family rule
+    # Gram partials + reduction + selection + combine, and with the peer-memory
+    # exchange (N > 1) the reduction is a reduce-and-store plus a gather kernel
+    peer = world > 1 and aggs["krum"]._use_peer_exchange(dev)
+    launches_per_step = 3 + 3 * (5 if peer else 4)
     # every stage class of the step (ms per step, rank 0): kernels plus the
     # exchange / select / gather stages of the d-sharded path
     stages = {c: round(t / args.steps, 4) for c, t in sorted(cls_ms.items())}
@@ -338,7 +343,7 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": int(per_launch_bytes),
                      "traffic": traffic_from_profiles(dom)},
         "kernels": kernels, "per_rule": per_rule, "clocks": clk.summary(),
-        "stages_ms": stages, "gpu_launches": 15 * args.steps, "e2e": e2e,
+        "stages_ms": stages, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, X, d)
