@@ -91,11 +91,32 @@ def rule_id(rule) -> int:
 _PTR_CACHE: dict = {}
 
 
+class DevicePtrRows:
+    """n gradient rows given by raw device addresses (ints), e.g. rows read in
+    place from other GPUs' memory over NVLink (dist.WorkerShards).  The
+    addresses must be 16-byte aligned and hold >= d fp32 values."""
+
+    def __init__(self, ptrs, device):
+        self.ptrs = [int(p) for p in ptrs]
+        self.device = torch.device(device)
+        self._arr = (ctypes.c_void_p * max(len(self.ptrs), 1))(*self.ptrs)
+
+    def __len__(self):
+        return len(self.ptrs)
+
+
 def row_pointers(grads, d: int | None = None):
     """(ctypes void* array, n, d) from a list of 1-D fp32 CUDA tensors or a
     2-D [n, ld] fp32 CUDA tensor with unit column stride.  For a matrix the
     row pointers are base + i * row_stride (no per-row tensor views), and the
     ctypes array is cached per (base, n, stride)."""
+    if isinstance(grads, DevicePtrRows):
+        n = len(grads)
+        if not 1 <= n <= MAX_N:
+            raise ValueError(f"n = {n} outside [1, {MAX_N}]")
+        if d is None:
+            raise ValueError("d is required with raw row addresses")
+        return grads._arr, n, d, grads.device
     if isinstance(grads, torch.Tensor):
         if grads.dim() != 2:
             raise ValueError("a gradient matrix must be 2-D [n, ld]")

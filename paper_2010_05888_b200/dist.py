@@ -237,7 +237,7 @@ class ShardedAggregator:
         cross-GPU barrier that makes the replicated output readable; the
         caller then calls sync() (any aggregator of the group) before reading
         it, and reads it before its next sync()."""
-        dev = rows_local.device if isinstance(rows_local, torch.Tensor) else rows_local[0].device
+        dev = rows_local.device if hasattr(rows_local, "device") else rows_local[0].device
         self._state(dev)
         mark = mark or (lambda label: None)
         if self.output in ("fused", "fused-mc") and self.world > 1:
@@ -308,3 +308,45 @@ class ShardedAggregator:
             return None
         from . import _lib
         return self._idx[: _lib.gar_num_selected(self.rule, self.n, self.f, self.m)]
+
+
+class WorkerShards:
+    """Worker-major input for the d-sharded GARs: in data
+    parallelism each GPU holds the FULL gradients of its own workers (worker
+    w lives on rank w mod world), while rank s aggregates coordinate slice s
+    of every worker's gradient.  Instead of an all-to-all into the d-sharded
+    layout, the gradients sit in one symmetric-memory buffer per rank and
+    rank s's kernels read slice s of each remote worker's row in place over
+    NVLink (their TMA bulk copies / loads take peer addresses), so the
+    exchange is fused into the aggregation kernels and needs no extra
+    memory.  fill local_rows(), call ready() on every rank, then pass
+    slice_rows(lo) to ShardedAggregator.aggregate."""
+
+    def __init__(self, n: int, d: int, group=None, device=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        from ._lib import DevicePtrRows
+        self._rows_cls = DevicePtrRows
+        self.n, self.d = int(n), int(d)
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.ld = (self.d + 3) // 4 * 4
+        self.local_workers = [w for w in range(self.n) if w % self.world == self.rank]
+        per_rank = (self.n + self.world - 1) // self.world
+        self.buf = symm_mem.empty(per_rank * self.ld, dtype=torch.float32, device=self.device)
+        self.handle = symm_mem.rendezvous(self.buf, self.group)
+        self.bases = [int(self.handle.buffer_ptrs[r]) for r in range(self.world)]
+
+    def local_rows(self) -> torch.Tensor:
+        """[len(local_workers), ld] view: row j is worker local_workers[j]."""
+        return self.buf[: len(self.local_workers) * self.ld].view(len(self.local_workers), self.ld)
+
+    def ready(self):
+        """Barrier: every rank's local rows are written and visible."""
+        self.handle.barrier()
+
+    def slice_rows(self, lo: int):
+        """The n rows of coordinates [lo, ...) as raw addresses, worker order."""
+        ptrs = [self.bases[w % self.world] + 4 * ((w // self.world) * self.ld + lo) for w in range(self.n)]
+        return self._rows_cls(ptrs, self.device)

@@ -58,7 +58,7 @@ class Aggregator:
         return t
 
     def _check_n(self, grads):
-        n = grads.shape[0] if isinstance(grads, torch.Tensor) else len(grads)
+        n = grads.shape[0] if isinstance(grads, torch.Tensor) else len(grads)   # tensors, lists, DevicePtrRows
         if n != self.n:
             raise ValueError(f"expected n = {self.n} gradients, got {n}")
 
