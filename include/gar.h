@@ -212,11 +212,16 @@ gar_status gar_combine_sgd(gar_rule rule, const float* const* grads, int n, int 
  *   zero before the first call, 4-byte aligned).
  * epoch: > the previous call's epoch, the same on every rank for one call.
  * world <= 8.  A rank that does not arrive within ~10 s yields NaN in
- * gram_dev instead of a hang.  workspace as for gar_gram_partial. */
+ * gram_dev instead of a hang.  workspace as for gar_gram_partial.
+ * stage_rows (optional, host array of n DEVICE fp32[d_local] buffers,
+ * 16-byte aligned): the Gram kernel also writes every row's slice there from
+ * its staging ring (bulk stores), so rows read from other GPUs' memory
+ * (worker-major ingress) land locally for the combine step
+ * while the Gram is computed; NULL to skip. */
 gar_status gar_gram_exchange(const float* const* grads, int n, int64_t d_local,
                              double* const* peer_slots, uint32_t* const* peer_flags, int rank,
-                             int world, uint32_t epoch, double* gram_dev, void* workspace,
-                             size_t workspace_bytes, gar_stream_t stream);
+                             int world, uint32_t epoch, double* gram_dev, float* const* stage_rows,
+                             void* workspace, size_t workspace_bytes, gar_stream_t stream);
 
 /* Trimmed-set membership (verification entry point for row a3, PAPER.md
  * l.316 footnote; the north_star's bit-exact "trimmed-set membership"): bit i

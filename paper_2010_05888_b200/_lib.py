@@ -58,7 +58,7 @@ def _load():
         "gar_aggregate_mcast": ([I, PP, I, I, I, I64, P, P, P, P, SZ, P], I),
         "gar_combine_mcast": ([I, PP, I, I, I, I64, P, P, P, P], I),
         "gar_trimmed_membership": ([PP, I, I, I64, P, P], I),
-        "gar_gram_exchange": ([PP, I, I64, PP, PP, I, I, ctypes.c_uint32, P, P, SZ, P], I),
+        "gar_gram_exchange": ([PP, I, I64, PP, PP, I, I, ctypes.c_uint32, P, PP, P, SZ, P], I),
         "gar_aggregate_sgd": ([I, PP, I, I, I, I64, P, ctypes.c_float, P, P, SZ, P], I),
         "gar_combine_sgd": ([I, PP, I, I, I, I64, P, P, ctypes.c_float, P], I),
     }
@@ -346,14 +346,20 @@ def gar_trimmed_membership(grads, f: int, mask: torch.Tensor, d: int | None = No
 
 
 def gar_gram_exchange(grads, gram: torch.Tensor, workspace: torch.Tensor, peer_slots, peer_flags, rank: int,
-                      world: int, epoch: int, d: int | None = None, stream=None):
+                      world: int, epoch: int, d: int | None = None, stream=None, stage: torch.Tensor | None = None):
     """Whole-vector Gram matrix of d-sharded rows, exchanged over peer memory
-    (ints peer_slots / peer_flags: every rank's slot / flag arrays)."""
+    (ints peer_slots / peer_flags: every rank's slot / flag arrays).  stage:
+    optional [n, >= d] fp32 matrix that receives a local copy of the rows."""
     arr, n, d, dev = row_pointers(grads, d)
     sl, _ = _ptr_array(peer_slots)
     fl, _ = _ptr_array(peer_flags)
     g = _buf(gram, torch.float64, n * n, dev, "gram")
-    check(lib.gar_gram_exchange(arr, n, d, sl, fl, rank, world, epoch, g, _ptr(workspace), _wsb(workspace),
+    st = None
+    if stage is not None:
+        if stage.dim() != 2 or stage.shape[0] != n or stage.shape[1] < d or stage.stride(1) != 1:
+            raise ValueError("stage must be an [n, >= d] row-major fp32 matrix")
+        st, _, _, _ = row_pointers(stage, d)
+    check(lib.gar_gram_exchange(arr, n, d, sl, fl, rank, world, epoch, g, st, _ptr(workspace), _wsb(workspace),
                                 stream_handle(dev, stream)), "gar_gram_exchange")
     return gram
 

@@ -502,7 +502,8 @@ gar_status gar_combine_sgd(gar_rule rule, const float* const* grads, int n, int 
 
 gar_status gar_gram_exchange(const float* const* grads, int n, int64_t d_local, double* const* peer_slots,
                              uint32_t* const* peer_flags, int rank, int world, uint32_t epoch, double* gram_dev,
-                             void* workspace, size_t workspace_bytes, gar_stream_t stream) {
+                             float* const* stage_rows, void* workspace, size_t workspace_bytes,
+                             gar_stream_t stream) {
   if (n < 1 || n > GAR_MAX_N || !gram_dev) return GAR_ERR_INVALID_ARGUMENT;
   if (world < 1 || world > gar::kMaxWorld || rank < 0 || rank >= world || !peer_slots || !peer_flags)
     return GAR_ERR_INVALID_ARGUMENT;
@@ -517,13 +518,15 @@ gar_status gar_gram_exchange(const float* const* grads, int n, int64_t d_local, 
   }
   gar_status s = check_rows(grads, n, d_local);
   if (s != GAR_OK) return s;
+  if (stage_rows && (s = check_rows(stage_rows, n, d_local)) != GAR_OK) return s;
   if (!workspace || workspace_bytes < ws_bytes_for(n)) return GAR_ERR_WORKSPACE;
   if ((s = check_device_rows(grads, n, nullptr)) != GAR_OK) return s;
   if ((s = check_device_ptr(gram_dev)) != GAR_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Workspace w = carve(workspace, n);
   int parts = 0;
-  if ((s = cuda_status(gar::launch_gram_partials(grads, n, d_local, w.partials, num_sms(), &parts, st))) != GAR_OK)
+  if ((s = cuda_status(gar::launch_gram_partials(grads, n, d_local, w.partials, num_sms(), &parts, st,
+                                                 stage_rows))) != GAR_OK)
     return s;
   return cuda_status(gar::launch_gram_exchange(w.partials, parts, n, slots, flags, world, rank, epoch, gram_dev, st));
 }

@@ -15,8 +15,11 @@ constexpr int kGramMaxParts = 160;
 
 // Partial Gram matrices of the centred rows, one fp64 [n x n] per CTA,
 // written to partials[p*n*n ...].  *n_parts receives the number written.
+// stage_rows (optional, n device pointers): every row's [0, d) is also copied
+// there from the kernel's staging ring (fused ingress staging).
 cudaError_t launch_gram_partials(const float* const* rows, int n, int64_t d, double* partials,
-                                 int num_sms, int* n_parts, cudaStream_t stream);
+                                 int num_sms, int* n_parts, cudaStream_t stream,
+                                 float* const* stage_rows = nullptr);
 
 // Reference-quality SIMT Gram (fp64 products); test/debug only.
 cudaError_t launch_gram_partials_simt(const float* const* rows, int n, int64_t d, double* partials,

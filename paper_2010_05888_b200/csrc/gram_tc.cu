@@ -247,7 +247,7 @@ __device__ int center_pick(const RowPtrs& rows, int n, int64_t d, int64_t k_begi
 template <int NP>
 __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
     gram_tc_kernel(const __grid_constant__ RowPtrs rows, int n, int64_t d, int64_t num_tiles,
-                   double* __restrict__ partials, int l2_hint) {
+                   double* __restrict__ partials, int l2_hint, const __grid_constant__ RowPtrs stage) {
   using C = Cfg<NP>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment (SWIZZLE_128B) by offsetting the shared array itself, so
@@ -368,6 +368,23 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
 #pragma unroll
       for (int q = 0; q < C::PROD_WARPS; ++q)
         mbar_wait(&raw_full[rs * C::PROD_WARPS + q], static_cast<uint32_t>(j / C::RAW_STAGES) & 1);
+      // fused ingress staging (gar_gram_exchange with stage rows): the landed
+      // raw stage -- rows that may live on other GPUs -- is also written to
+      // this GPU's stage buffers by bulk stores, so the combine that follows
+      // reads local memory; the transfer overlaps the Gram tile by tile
+      if (stage.p[0] != nullptr && warp == 0 && lane == 0) {
+        const int64_t k0 = t0 * C::KT + j * C::RAW_KT;
+        const int64_t k_end = ((t0 + T) * C::KT < d) ? (t0 + T) * C::KT : d;
+        const int64_t cnt = (k_end - k0 < C::RAW_KT) ? k_end - k0 : C::RAW_KT;
+        const uint32_t bytes = static_cast<uint32_t>(cnt & ~int64_t(3)) * 4u;
+        if (bytes) {
+          for (int r = 0; r < n; ++r)
+            bulk_s2g(const_cast<float*>(stage.p[r]) + k0, raw + rs * C::RAW_BYTES + r * C::RAW_PITCH, bytes);
+          bulk_commit();
+        }
+        for (int64_t k = k0 + (cnt & ~int64_t(3)); k < k0 + cnt; ++k)   // ragged tail: < 4 coordinates
+          for (int r = 0; r < n; ++r) const_cast<float*>(stage.p[r])[k] = rows.p[r][k];
+      }
 #pragma unroll
       for (int sub = 0; sub < C::RAW_SUB; ++sub) {
         const int64_t i = j * C::RAW_SUB + sub;
@@ -445,9 +462,11 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&op_full[s]);
       }
+      if (stage.p[0] != nullptr && warp == 0 && lane == 0) bulk_wait_read0();   // stage read out before reuse
       __syncwarp();
       if (lane == 0) mbar_arrive(&raw_empty[rs]);
     }
+    if (stage.p[0] != nullptr && warp == 0 && lane == 0) bulk_wait0();
   } else if (warp == C::MMA_WARP) {
     // ====================================================== MMA issuer
     if (lane == 0) {
@@ -541,7 +560,7 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
 
 template <int NP>
 cudaError_t launch_np(const RowPtrs& rp, int n, int64_t d, double* partials, int num_sms, int* n_parts,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, const RowPtrs& stage) {
   using C = Cfg<NP>;
   const int64_t tiles = (d + C::KT - 1) / C::KT;
   int grid = num_sms < kGramMaxParts ? num_sms : kGramMaxParts;
@@ -550,7 +569,7 @@ cudaError_t launch_np(const RowPtrs& rp, int n, int64_t d, double* partials, int
   cudaError_t e = cached_occupancy(gram_tc_kernel<NP>, C::THREADS, C::SMEM_BYTES, &occ);
   if (e != cudaSuccess) return e;
   gram_tc_kernel<NP><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(rp, n, d, tiles, partials,
-                                                                   l2_evict_first_enabled());
+                                                                   l2_evict_first_enabled(), stage);
   *n_parts = grid;
   return cudaGetLastError();
 }
@@ -558,13 +577,16 @@ cudaError_t launch_np(const RowPtrs& rp, int n, int64_t d, double* partials, int
 }  // namespace
 
 cudaError_t launch_gram_partials(const float* const* rows, int n, int64_t d, double* partials, int num_sms,
-                                 int* n_parts, cudaStream_t stream) {
-  RowPtrs rp;
-  for (int i = 0; i < GAR_MAX_N; ++i) rp.p[i] = (i < n) ? rows[i] : nullptr;
-  if (n <= 8) return launch_np<8>(rp, n, d, partials, num_sms, n_parts, stream);
-  if (n <= 16) return launch_np<16>(rp, n, d, partials, num_sms, n_parts, stream);
-  if (n <= 32) return launch_np<32>(rp, n, d, partials, num_sms, n_parts, stream);
-  return launch_np<64>(rp, n, d, partials, num_sms, n_parts, stream);
+                                 int* n_parts, cudaStream_t stream, float* const* stage_rows) {
+  RowPtrs rp, st;
+  for (int i = 0; i < GAR_MAX_N; ++i) {
+    rp.p[i] = (i < n) ? rows[i] : nullptr;
+    st.p[i] = (stage_rows && i < n) ? stage_rows[i] : nullptr;
+  }
+  if (n <= 8) return launch_np<8>(rp, n, d, partials, num_sms, n_parts, stream, st);
+  if (n <= 16) return launch_np<16>(rp, n, d, partials, num_sms, n_parts, stream, st);
+  if (n <= 32) return launch_np<32>(rp, n, d, partials, num_sms, n_parts, stream, st);
+  return launch_np<64>(rp, n, d, partials, num_sms, n_parts, stream, st);
 }
 
 }  // namespace gar

@@ -72,8 +72,8 @@ class _LibgarBackend:
     def select_from_gram(self, rule, gram, n, f, m, idx, ws=None):
         return self._lib.gar_select_from_gram(rule, gram, n, f, m, idx, workspace=ws)
 
-    def gram_exchange(self, rows, gram, ws, d, slots, flags, rank, world, epoch):
-        self._lib.gar_gram_exchange(rows, gram, ws, slots, flags, rank, world, epoch, d=d)
+    def gram_exchange(self, rows, gram, ws, d, slots, flags, rank, world, epoch, stage=None):
+        self._lib.gar_gram_exchange(rows, gram, ws, slots, flags, rank, world, epoch, d=d, stage=stage)
 
     def combine(self, rule, rows, f, m, idx, out, d, extra=()):
         if isinstance(extra, Multicast):
@@ -162,6 +162,18 @@ class ShardedAggregator:
         self._calls += 1
         return self._symm[self._calls % 2]
 
+    def _stage_for(self, rows_local, dev):
+        """Rows given as raw (possibly remote) addresses and read twice by a
+        Krum-family rule (Gram, then combine): a local [n, d_local] staging
+        matrix the Gram kernel fills on the way, or None."""
+        from ._lib import DevicePtrRows
+        if not isinstance(rows_local, DevicePtrRows) or not self._use_peer_exchange(dev):
+            return None
+        ld = (self.d_local + 3) // 4 * 4
+        if getattr(self, "_stage", None) is None or self._stage.shape[1] < ld:
+            self._stage = torch.empty((self.n, ld), dtype=torch.float32, device=dev)
+        return self._stage
+
     def _use_peer_exchange(self, device) -> bool:
         if self.world <= 1 or self.rule not in KRUM_FAMILY or device.type != "cuda":
             return False
@@ -187,8 +199,9 @@ class ShardedAggregator:
             self._xchg = {"buf": buf, "handle": handle, "bases": bases, "slot_bytes": slot_bytes, "epoch": 0}
         return self._xchg
 
-    def _gram_whole(self, rows_local, dev, mark):
-        """Whole-vector Gram matrix on every rank (self._gram)."""
+    def _gram_whole(self, rows_local, dev, mark, stage=None):
+        """Whole-vector Gram matrix on every rank (self._gram); with `stage`
+        the Gram kernel also copies the rows there (fused ingress staging)."""
         if self._use_peer_exchange(dev):
             x = self._exchange_buffers(dev)
             x["epoch"] += 1
@@ -196,7 +209,7 @@ class ShardedAggregator:
             slots = [b + par * x["slot_bytes"] for b in x["bases"]]
             flags = [b + 2 * x["slot_bytes"] for b in x["bases"]]
             self.backend.gram_exchange(rows_local, self._gram, self._ws, self.d_local, slots, flags, self.rank,
-                                       self.world, x["epoch"])
+                                       self.world, x["epoch"], stage=stage)
             mark("gram")
             mark("exchange")
             return
@@ -245,10 +258,12 @@ class ShardedAggregator:
         if out_local is None:
             out_local = torch.empty(self.d_local, dtype=torch.float32, device=dev)
         if self.rule in KRUM_FAMILY:
-            self._gram_whole(rows_local, dev, mark)
+            stage = self._stage_for(rows_local, dev)
+            self._gram_whole(rows_local, dev, mark, stage)
             self.backend.select_from_gram(self.rule, self._gram, self.n, self.f, self.m, self._idx, ws=self._ws)
             mark("select")
-            self.backend.combine(self.rule, rows_local, self.f, self.m, self._idx, out_local, self.d_local)
+            self.backend.combine(self.rule, stage if stage is not None else rows_local, self.f, self.m, self._idx,
+                                 out_local, self.d_local)
             mark("combine")
         else:
             self.backend.coordinatewise(self._agg, rows_local, out_local, self.d_local)
@@ -288,10 +303,12 @@ class ShardedAggregator:
         buf, handle, extra = self._fused_buffers(dev)
         out_local = buf[self.lo: self.hi]
         if self.rule in KRUM_FAMILY:
-            self._gram_whole(rows_local, dev, mark)
+            stage = self._stage_for(rows_local, dev)
+            self._gram_whole(rows_local, dev, mark, stage)
             self.backend.select_from_gram(self.rule, self._gram, self.n, self.f, self.m, self._idx, ws=self._ws)
             mark("select")
-            self.backend.combine(self.rule, rows_local, self.f, self.m, self._idx, out_local, self.d_local, extra)
+            self.backend.combine(self.rule, stage if stage is not None else rows_local, self.f, self.m, self._idx,
+                                 out_local, self.d_local, extra)
             mark("combine")
         else:
             self.backend.coordinatewise_bcast(self._agg, rows_local, out_local, self.d_local, extra)

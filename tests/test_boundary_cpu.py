@@ -166,7 +166,7 @@ def test_gram_exchange_checks_its_peer_arrays(gl):
     def call(slots, flags, rank, world):
         sa = (ctypes.c_void_p * max(len(slots), 1))(*slots)
         fa = (ctypes.c_void_p * max(len(flags), 1))(*flags)
-        return gl.lib.gar_gram_exchange(ptrs, n, 100, sa, fa, rank, world, 1, ctypes.c_void_p(0x50_0000),
+        return gl.lib.gar_gram_exchange(ptrs, n, 100, sa, fa, rank, world, 1, ctypes.c_void_p(0x50_0000), None,
                                         ctypes.c_void_p(0x60_0000), 1 << 30, None)
     ok_s, ok_f = [0x70_0000, 0x71_0000], [0x72_0000, 0x73_0000]
     assert call(ok_s, ok_f, 2, 2) == 1                  # rank outside [0, world)
