@@ -21,10 +21,6 @@ cudaError_t launch_gram_partials(const float* const* rows, int n, int64_t d, dou
                                  int num_sms, int* n_parts, cudaStream_t stream,
                                  float* const* stage_rows = nullptr);
 
-// Reference-quality SIMT Gram (fp64 products); test/debug only.
-cudaError_t launch_gram_partials_simt(const float* const* rows, int n, int64_t d, double* partials,
-                                      int num_sms, int* n_parts, cudaStream_t stream);
-
 // G = sum_p partials[p] in fixed order p = 0..n_parts-1 (deterministic).
 cudaError_t launch_gram_reduce(const double* partials, int n_parts, int n, double* G,
                                cudaStream_t stream);
