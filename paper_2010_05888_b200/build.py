@@ -58,8 +58,10 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
         if not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), hdr_mtime):
             todo.append((s, o, o[:-2] + ".log"))
     stale = [o for o in glob.glob(os.path.join(OBJ, "*.o")) if o not in objs]
-    for o in stale:
+    for o in stale:                       # a removed source: drop its object and log, and relink below
         os.remove(o)
+        if os.path.exists(o[:-2] + ".log"):
+            os.remove(o[:-2] + ".log")
     if todo:
         jobs = jobs or max(1, os.cpu_count() or 1)
         if verbose:
@@ -68,7 +70,7 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
             for o in ex.map(lambda t: _compile(*t), todo):
                 if verbose:
                     print(f"[libgar]   {os.path.basename(o)}", flush=True)
-    if todo or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
+    if todo or stale or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         tmp = LIB + f".tmp{os.getpid()}"
         subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcuda"])
         os.replace(tmp, LIB)
