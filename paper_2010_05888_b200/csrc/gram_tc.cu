@@ -244,7 +244,9 @@ __device__ int center_pick(const RowPtrs& rows, int n, int64_t d, int64_t k_begi
   return best;
 }
 
-template <int NP>
+// STAGE: the fused ingress staging variant (stage rows given); a separate
+// instantiation so the plain Gram carries none of its code.
+template <int NP, bool STAGE>
 __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
     gram_tc_kernel(const __grid_constant__ RowPtrs rows, int n, int64_t d, int64_t num_tiles,
                    double* __restrict__ partials, int l2_hint, const __grid_constant__ RowPtrs stage) {
@@ -372,7 +374,7 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
       // raw stage -- rows that may live on other GPUs -- is also written to
       // this GPU's stage buffers by bulk stores, so the combine that follows
       // reads local memory; the transfer overlaps the Gram tile by tile
-      if (stage.p[0] != nullptr && warp == 0 && lane == 0) {
+      if (STAGE && warp == 0 && lane == 0) {
         const int64_t k0 = t0 * C::KT + j * C::RAW_KT;
         const int64_t k_end = ((t0 + T) * C::KT < d) ? (t0 + T) * C::KT : d;
         const int64_t cnt = (k_end - k0 < C::RAW_KT) ? k_end - k0 : C::RAW_KT;
@@ -462,11 +464,11 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&op_full[s]);
       }
-      if (stage.p[0] != nullptr && warp == 0 && lane == 0) bulk_wait_read0();   // stage read out before reuse
+      if (STAGE && warp == 0 && lane == 0) bulk_wait_read0();   // stage read out before reuse
       __syncwarp();
       if (lane == 0) mbar_arrive(&raw_empty[rs]);
     }
-    if (stage.p[0] != nullptr && warp == 0 && lane == 0) bulk_wait0();
+    if (STAGE && warp == 0 && lane == 0) bulk_wait0();
   } else if (warp == C::MMA_WARP) {
     // ====================================================== MMA issuer
     if (lane == 0) {
@@ -566,10 +568,11 @@ cudaError_t launch_np(const RowPtrs& rp, int n, int64_t d, double* partials, int
   int grid = num_sms < kGramMaxParts ? num_sms : kGramMaxParts;
   if (tiles < grid) grid = static_cast<int>(tiles > 0 ? tiles : 1);
   int occ = 0;
-  cudaError_t e = cached_occupancy(gram_tc_kernel<NP>, C::THREADS, C::SMEM_BYTES, &occ);
+  const bool staged = stage.p[0] != nullptr;
+  auto kern = staged ? gram_tc_kernel<NP, true> : gram_tc_kernel<NP, false>;
+  cudaError_t e = cached_occupancy(kern, C::THREADS, C::SMEM_BYTES, &occ);
   if (e != cudaSuccess) return e;
-  gram_tc_kernel<NP><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(rp, n, d, tiles, partials,
-                                                                   l2_evict_first_enabled(), stage);
+  kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(rp, n, d, tiles, partials, l2_evict_first_enabled(), stage);
   *n_parts = grid;
   return cudaGetLastError();
 }
