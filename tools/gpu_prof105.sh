@@ -1,0 +1,10 @@
+cd $GRAFT_REPO_ROOT
+NCU=/usr/local/cuda/bin/ncu
+timeout 600 python bench.py > gpurun_out/r105_bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/r105_bench.log
+CMD="python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline"
+timeout 600 $CMD > gpurun_out/r105_short.log 2>&1 && \
+timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r105_launches.csv $CMD > gpurun_out/r105_ncu_launch.log 2>&1
+echo "launch rc=$?" >> gpurun_out/r105_short.log
+timeout 300 python tools/prof_step.py > gpurun_out/r105_plain.log 2>&1 && \
+timeout 1500 $NCU --set full --clock-control none --import-source on -k "regex:gram_tc|coord_select|coord_ldg|copy_row" -s 9 -c 9 -o gpurun_out/r105_full python tools/prof_step.py > gpurun_out/r105_ncu_full.log 2>&1
+echo "full rc=$?" >> gpurun_out/r105_plain.log
