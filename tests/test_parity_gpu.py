@@ -241,6 +241,43 @@ def test_mean_around_median_parity(gar, n, f):
     assert_same_bits(out.cpu().numpy(), oracle.mean_around_median(x, f), "mean around median")
 
 
+@pytest.mark.parametrize("n,d", [(7, 100_003), (31, 300_001), (64, 20_003)])
+def test_gram_exchange_single_rank_and_staging(gar, n, d):
+    """gar_gram_exchange with world = 1 (slots and flags in this GPU's memory):
+    the flag handshake completes, G equals gar_gram_partial's bit for bit, and
+    the staging copy (the fused ingress of the d-sharded path) equals the rows."""
+    x = synth.make_gradients(n, (n - 3) // 4 if n >= 3 else 0, d, seed=5 + n, ld=d).numpy()
+    X = to_device(x)
+    ws = torch.empty(gar.gar_workspace_bytes("krum", n, 0, d), dtype=torch.uint8, device="cuda")
+    G0 = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    gar.gar_gram_partial(X, G0, ws, d=d)
+    slots = torch.zeros(n * n, dtype=torch.float64, device="cuda")
+    flags = torch.zeros(4, dtype=torch.int32, device="cuda")
+    stage = torch.full((n, (d + 3) // 4 * 4), float("nan"), dtype=torch.float32, device="cuda")
+    G1 = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    for epoch in (1, 2):
+        gar.gar_gram_exchange(X, G1, ws, [slots.data_ptr()], [flags.data_ptr()], 0, 1, epoch, d=d, stage=stage)
+        torch.cuda.synchronize()
+        assert torch.equal(G0, G1), epoch
+    assert int(flags[0]) == 2
+    assert torch.equal(stage[:, :d], X[:, :d])
+
+
+def test_raw_address_rows(gar):
+    """Rows given as raw device addresses (_lib.DevicePtrRows, the form the
+    worker-major ingress uses for peer rows) aggregate exactly like the matrix."""
+    from paper_2010_05888_b200._lib import DevicePtrRows
+    n, f, d = 19, 4, 50_001
+    X = to_device(synth.make_gradients(n, f, d, seed=8, ld=d).numpy())
+    rows = DevicePtrRows([X.data_ptr() + i * X.stride(0) * 4 for i in range(n)], X.device)
+    for rule in RULES:
+        a = gar.init(rule, n, f)
+        ref = a.aggregate(X, out=torch.empty(d, dtype=torch.float32, device="cuda"), d=d)
+        got = a.aggregate(rows, out=torch.empty(d, dtype=torch.float32, device="cuda"), d=d)
+        torch.cuda.synchronize()
+        assert_same_bits(got.cpu().numpy(), ref.cpu().numpy(), rule)
+
+
 def test_binding_rejects_bad_buffers(gar):
     """The binding checks what the C ABI cannot: dtype, device, size."""
     n, f, d = 7, 1, 1000
