@@ -223,6 +223,14 @@ gar_status gar_gram_exchange(const float* const* grads, int n, int64_t d_local,
                              int world, uint32_t epoch, double* gram_dev, float* const* stage_rows,
                              void* workspace, size_t workspace_bytes, gar_stream_t stream);
 
+/* Non-finite rows (the vector-level sanitize that counts
+ * non-finite payloads toward f): *mask_dev (DEVICE uint64,
+ * 8-byte aligned) <- bit i set iff row i holds a NaN or +-inf in [0, d).
+ * Reads every input once.  The caller drops those rows and aggregates the
+ * rest with f reduced by their count (paper_2010_05888_b200.sanitize). */
+gar_status gar_nonfinite_rows(const float* const* grads, int n, int64_t d, uint64_t* mask_dev,
+                              gar_stream_t stream);
+
 /* Trimmed-set membership (verification entry point for row a3, PAPER.md
  * l.316 footnote; the north_star's bit-exact "trimmed-set membership"): bit i
  * of mask_dev[k] is set iff input i is among the n - 2f values the trimmed

@@ -248,6 +248,16 @@ def mean_around_median(x, f, threads=None):
     return out
 
 
+def sanitize(x, f):
+    """(kept, excluded) input indices; a row is excluded iff it
+    holds a non-finite value; more than f excluded -> OracleError(2)."""
+    x = _f32(x)
+    bad = [i for i in range(x.shape[0]) if not np.all(np.isfinite(x[i]))]
+    if len(bad) > f:
+        raise OracleError(2, "sanitize (TooManyNonFinite)")
+    return [i for i in range(x.shape[0]) if i not in bad], bad
+
+
 def mda_select(D, f):
     """Indices (ascending) of the size n-f subset of minimum diameter
     (max pairwise squared distance), ties to the lexicographically smallest set."""

@@ -58,6 +58,7 @@ def _load():
         "gar_aggregate_mcast": ([I, PP, I, I, I, I64, P, P, P, P, SZ, P], I),
         "gar_combine_mcast": ([I, PP, I, I, I, I64, P, P, P, P], I),
         "gar_trimmed_membership": ([PP, I, I, I64, P, P], I),
+        "gar_nonfinite_rows": ([PP, I, I64, P, P], I),
         "gar_gram_exchange": ([PP, I, I64, PP, PP, I, I, ctypes.c_uint32, P, PP, P, SZ, P], I),
         "gar_aggregate_sgd": ([I, PP, I, I, I, I64, P, ctypes.c_float, P, P, SZ, P], I),
         "gar_combine_sgd": ([I, PP, I, I, I, I64, P, P, ctypes.c_float, P], I),
@@ -381,3 +382,11 @@ def gar_combine_sgd(rule, grads, f: int, m: int, indices: torch.Tensor, params: 
     check(lib.gar_combine_sgd(rule_id(rule), arr, n, f, m, d, ix, pp, float(lr), stream_handle(dev, stream)),
           "gar_combine_sgd")
     return params
+
+
+def gar_nonfinite_rows(grads, mask: torch.Tensor, d: int | None = None, stream=None):
+    """mask: device int64[>= 1]; mask[0] bit i set iff row i holds a NaN/inf."""
+    arr, n, d, dev = row_pointers(grads, d)
+    mk = _buf(mask, (torch.int64, torch.uint64), 1, dev, "mask")
+    check(lib.gar_nonfinite_rows(arr, n, d, mk, stream_handle(dev, stream)), "gar_nonfinite_rows")
+    return mask

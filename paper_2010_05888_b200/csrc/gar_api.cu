@@ -531,6 +531,17 @@ gar_status gar_gram_exchange(const float* const* grads, int n, int64_t d_local, 
   return cuda_status(gar::launch_gram_exchange(w.partials, parts, n, slots, flags, world, rank, epoch, gram_dev, st));
 }
 
+gar_status gar_nonfinite_rows(const float* const* grads, int n, int64_t d, uint64_t* mask_dev,
+                              gar_stream_t stream) {
+  if (n < 1 || n > GAR_MAX_N || !mask_dev) return GAR_ERR_INVALID_ARGUMENT;
+  if (reinterpret_cast<uintptr_t>(mask_dev) & 7u) return GAR_ERR_ALIGNMENT;
+  gar_status s = check_rows(grads, n, d);
+  if (s != GAR_OK) return s;
+  if ((s = check_device_rows(grads, n, mask_dev)) != GAR_OK) return s;
+  return cuda_status(gar::launch_nonfinite_rows(grads, n, d, mask_dev, num_sms(),
+                                                reinterpret_cast<cudaStream_t>(stream)));
+}
+
 gar_status gar_trimmed_membership(const float* const* grads, int n, int f, int64_t d, uint64_t* mask_dev,
                                   gar_stream_t stream) {
   gar_status s = check_rule_args(GAR_TRIMMED_MEAN, n, f, 0);

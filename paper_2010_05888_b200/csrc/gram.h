@@ -53,6 +53,10 @@ size_t mda_workspace_bytes(int n);
 cudaError_t launch_mda_select(const double* D, int n, int f, void* scratch, int num_sms, int32_t* idx_out,
                               cudaStream_t stream);
 
+// Rows with a non-finite value (membership.cu; SPEC's vector-level sanitize).
+cudaError_t launch_nonfinite_rows(const float* const* rows, int n, int64_t d, uint64_t* mask, int num_sms,
+                                  cudaStream_t stream);
+
 // Trimmed-set membership masks (membership.cu; verification entry point).
 cudaError_t launch_trimmed_membership(const float* const* rows, int n, int f, int64_t d, uint64_t* mask,
                                       int num_sms, cudaStream_t stream);

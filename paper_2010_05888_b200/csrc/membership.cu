@@ -30,7 +30,40 @@ __global__ void __launch_bounds__(256) trimmed_membership_kernel(const __grid_co
   }
 }
 
+// Rows holding any non-finite value (SPEC's vector-level sanitize):
+// blockIdx.y = row, grid-stride float4 chunks, one warp vote and at most one
+// atomicOr per warp.  Reads every input byte once (HBM-bound).
+__global__ void __launch_bounds__(256) nonfinite_rows_kernel(const __grid_constant__ RowPtrs rows, int64_t d,
+                                                             unsigned long long* __restrict__ mask) {
+  const int r = blockIdx.y;
+  const float* row = rows.p[r];
+  bool bad = false;
+  const int64_t n4 = d >> 2;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n4; q += int64_t(gridDim.x) * blockDim.x) {
+    const float4 v = __ldcs(reinterpret_cast<const float4*>(row) + q);
+    bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+  }
+  const int64_t k = (n4 << 2) + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (blockIdx.x == 0 && k < d) bad |= !isfinite(row[k]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(mask, 1ull << r);
+}
+
 }  // namespace
+
+cudaError_t launch_nonfinite_rows(const float* const* rows, int n, int64_t d, uint64_t* mask, int num_sms,
+                                  cudaStream_t stream) {
+  RowPtrs rp;
+  for (int i = 0; i < GAR_MAX_N; ++i) rp.p[i] = (i < n) ? rows[i] : nullptr;
+  cudaError_t e = cudaMemsetAsync(mask, 0, sizeof(uint64_t), stream);
+  if (e != cudaSuccess) return e;
+  int64_t bx = (d / 4 + 255) / 256;
+  const int64_t cap = (int64_t(num_sms) * 8 + n - 1) / n;
+  if (bx > cap) bx = cap;
+  if (bx < 1) bx = 1;
+  nonfinite_rows_kernel<<<dim3(static_cast<unsigned>(bx), n), 256, 0, stream>>>(
+      rp, d, reinterpret_cast<unsigned long long*>(mask));
+  return cudaGetLastError();
+}
 
 cudaError_t launch_trimmed_membership(const float* const* rows, int n, int f, int64_t d, uint64_t* mask,
                                       int num_sms, cudaStream_t stream) {

@@ -124,6 +124,47 @@ class Aggregator:
         return sh[key].aggregate(rows_local)
 
 
+class TooManyNonFinite(ValueError):
+    """more than f inputs hold non-finite values."""
+
+
+def sanitize(grads, f: int, d: int | None = None, stream=None):
+    """SPEC S:43-51 (vector-level sanitize): (kept, excluded)
+    input indices, excluded = the rows holding any NaN / +-inf, found by
+    gar_nonfinite_rows on the GPU (one pass over the inputs, then one 8-byte
+    read back to the host).  Raises TooManyNonFinite if more than f."""
+    arr, n, d, dev = _lib.row_pointers(grads, d)
+    mask = torch.zeros(1, dtype=torch.int64, device=dev)
+    _lib.gar_nonfinite_rows(grads, mask, d=d, stream=stream)
+    m = int(mask.item()) & ((1 << 64) - 1)
+    excluded = [i for i in range(n) if (m >> i) & 1]
+    if len(excluded) > f:
+        raise TooManyNonFinite(f"{len(excluded)} inputs hold non-finite values, more than f = {f}")
+    return [i for i in range(n) if not (m >> i) & 1], excluded
+
+
+def _select_rows(grads, idx):
+    if isinstance(grads, torch.Tensor):
+        base, rs = grads.data_ptr(), grads.stride(0) * 4
+        return _lib.DevicePtrRows([base + i * rs for i in idx], grads.device)
+    if isinstance(grads, _lib.DevicePtrRows):
+        return _lib.DevicePtrRows([grads.ptrs[i] for i in idx], grads.device)
+    return [grads[i] for i in idx]
+
+
+def aggregate_sanitized(agg: "Aggregator", grads, out: torch.Tensor | None = None, d: int | None = None):
+    """SPEC's AggregationOutcome path: drop the non-finite inputs (they count
+    toward f: the rule runs on n - e inputs with f - e), aggregate the rest.
+    Returns (out, excluded indices)."""
+    kept, excluded = sanitize(grads, agg.f, d)
+    if not excluded:
+        return agg.aggregate(grads, out=out, d=d), excluded
+    e = len(excluded)
+    sub = Aggregator(agg.rule, agg.n - e, agg.f - e, (agg.m or None) if agg.rule == "multi_krum" else None)
+    return sub.aggregate(_select_rows(grads, kept), out=out, d=d if d is not None else _lib.row_pointers(grads)[2]), \
+        excluded
+
+
 def init(name: str, n: int, f: int, m: int | None = None) -> Aggregator:
     """"The init() function takes the name of the required GAR
     (e.g., "median"), the value of n, the total number of inputs, and f"."""

@@ -475,3 +475,12 @@ def test_mean_around_median_pins():
         for v in kept:
             s += v
         assert np.float32(s / len(kept)) == oracle.mean_around_median(x, 2)[k]
+
+
+def test_sanitize_spec_examples():
+    """SPEC S:49-51."""
+    nan, inf = np.nan, np.inf
+    assert oracle.sanitize(np.array([[1, 2], [3, 4]], np.float32), 0) == ([0, 1], [])
+    assert oracle.sanitize(np.array([[1, 2], [nan, 4], [5, 6]], np.float32), 1) == ([0, 2], [1])
+    with pytest.raises(oracle.OracleError):
+        oracle.sanitize(np.array([[nan, 1], [1, inf]], np.float32), 1)

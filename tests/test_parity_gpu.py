@@ -278,6 +278,41 @@ def test_raw_address_rows(gar):
         assert_same_bits(got.cpu().numpy(), ref.cpu().numpy(), rule)
 
 
+@pytest.mark.parametrize("rule", ["median", "trimmed_mean", "multi_krum", "bulyan", "mda"])
+def test_sanitize_and_aggregate(gar, rule):
+    """SPEC S:43-51 on the GPU: gar_nonfinite_rows finds exactly the rows
+    with a NaN / inf (SPEC examples included); aggregate_sanitized runs the rule
+    on the rest with f reduced by their count, equal to the oracle's."""
+    X = to_device(np.array([[1, 2], [np.nan, 4], [5, 6]], np.float32))
+    assert gar.sanitize(X, 1, d=2) == ([0, 2], [1])
+    with pytest.raises(gar.TooManyNonFinite):
+        gar.sanitize(to_device(np.array([[np.nan, 1], [1, np.inf]], np.float32)), 1, d=2)
+    n, f, d = 15, 3, 10_003
+    x = synth.make_gradients(n, f, d, seed=41, ld=d).numpy()
+    x[4, 77] = np.inf
+    x[9, d - 1] = np.nan
+    X = to_device(x)
+    a = gar.init(rule, n, f)
+    out, excluded = gar.aggregate_sanitized(a, X, d=d)
+    torch.cuda.synchronize()
+    kept, bad = oracle.sanitize(x, f)
+    assert excluded == bad == [4, 9]
+    xs, fs = x[kept], f - len(bad)
+    if rule == "median":
+        ref = oracle.median(xs, fs)
+    elif rule == "trimmed_mean":
+        ref = oracle.trimmed_mean(xs, fs)
+    elif rule == "multi_krum":
+        ref = oracle.multi_krum(xs, fs)[0]
+    elif rule == "bulyan":
+        ref = oracle.bulyan(xs, fs)[0]
+    else:
+        ref = oracle.mda(xs, fs)[0]
+    np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-6, atol=1e-9)
+    if rule in ("median", "trimmed_mean"):
+        assert_same_bits(out.cpu().numpy(), ref, rule)
+
+
 def test_binding_rejects_bad_buffers(gar):
     """The binding checks what the C ABI cannot: dtype, device, size."""
     n, f, d = 7, 1, 1000
