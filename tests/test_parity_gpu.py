@@ -425,6 +425,32 @@ def test_determinism(gar):
             assert sa.tolist() == sb.tolist()
 
 
+def test_empty_and_degenerate_sizes(gar):
+    """d = 0 (nothing to aggregate: every rule succeeds and writes nothing;
+    selections come from an all-zero distance matrix, i.e. index order),
+    n = 1 (every coordinate-wise rule copies the row), d = 1 and d = 3 (all
+    ragged, no bulk copy at all)."""
+    n, f = 11, 2
+    X = torch.zeros((n, 4), dtype=torch.float32, device="cuda")
+    for rule in RULES:
+        a = gar.init(rule, n, f)
+        sentinel = torch.full((4,), 7.0, device="cuda")
+        a.aggregate(X, out=sentinel, d=0)
+        torch.cuda.synchronize()
+        assert torch.all(sentinel == 7.0), rule
+        if rule in KRUM_FAMILY:
+            assert a.select(X, d=0).cpu().tolist() == list(range(a.num_selected)), rule
+    v = np.random.default_rng(1).standard_normal((1, 1001)).astype(np.float32)
+    for rule in ("average", "median", "trimmed_mean", "mean_around_median"):
+        out = gar.init(rule, 1, 0).aggregate(to_device(v), d=1001)
+        torch.cuda.synchronize()
+        assert_same_bits(out.cpu().numpy(), v[0] + np.float32(0), rule)
+    for d in (1, 3):
+        x = np.random.default_rng(d).standard_normal((n, d)).astype(np.float32)
+        for rule in RULES:
+            check_rule(gar, rule, x, f)
+
+
 def test_errors_from_python(gar):
     X = to_device(np.zeros((8, 16), np.float32))
     with pytest.raises(gar.GarError):
