@@ -11,8 +11,12 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t a) {
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+// kind::i8: D s32 (c_format 2), A/B signed 8-bit (format 1), K-major
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 
-template <int N, bool ATMEM>
+template <int N, bool ATMEM, bool I8 = false>
 __global__ void bench(int iters, long long* out) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ uint32_t slot;
@@ -35,7 +39,7 @@ __global__ void bench(int iters, long long* out) {
   const uint32_t tb = slot;
   if (threadIdx.x == 0) {
     const uint32_t a0 = smem_u32(base), b0 = smem_u32(base + 64 * 1024);
-    constexpr uint32_t id = idesc_tf32(128, N);
+    constexpr uint32_t id = I8 ? idesc_i8(128, N) : idesc_tf32(128, N);
     uint32_t phase = 0;
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
@@ -46,6 +50,11 @@ __global__ void bench(int iters, long long* out) {
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
                        ::"r"(tb + 256), "r"(tb + 8 * (kk & 7)), "l"(bd), "r"(id), "r"(acc));
+        } else if (I8) {
+          const uint64_t ad = sw128_desc(a0 + (kk & 3) * 32 + (kk >> 2) * 16384);
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+                       ::"r"(tb + 256), "l"(ad), "l"(bd), "r"(id), "r"(acc));
         } else {
           const uint64_t ad = sw128_desc(a0 + (kk & 3) * 32 + (kk >> 2) * 16384);
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -66,25 +75,26 @@ __global__ void bench(int iters, long long* out) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(512));
 }
 
-template <int N, bool AT>
+template <int N, bool AT, bool I8 = false>
 void run() {
   long long* d; cudaMalloc(&d, 148 * 8);
   const int smem = 100 * 1024;
-  cudaFuncSetAttribute(bench<N, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(bench<N, AT, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
-  bench<N, AT><<<148, 128, smem>>>(iters, d);
-  bench<N, AT><<<148, 128, smem>>>(iters, d);
+  bench<N, AT, I8><<<148, 128, smem>>>(iters, d);
+  bench<N, AT, I8><<<148, 128, smem>>>(iters, d);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double cyc = (double)h[0] / (iters * 16);
-  double macs = 128.0 * N * 8;
-  printf("tf32 M=128 N=%3d K=8 A from %s: %6.1f cycles/MMA, %6.0f MAC/clk/SM (%s)\n", N, AT ? "TMEM" : "smem", cyc,
-         macs / cyc, cudaGetErrorString(e));
+  double macs = 128.0 * N * (I8 ? 32 : 8);
+  printf("%s M=128 N=%3d K=%d A from %s: %6.1f cycles/MMA, %6.0f MAC/clk/SM (%s)\n", I8 ? "i8  " : "tf32", N,
+         I8 ? 32 : 8, AT ? "TMEM" : "smem", cyc, macs / cyc, cudaGetErrorString(e));
   cudaFree(d);
 }
 
 int main() {
   run<64, false>(); run<128, false>(); run<256, false>();
   run<64, true>(); run<128, true>(); run<256, true>();
+  run<64, false, true>(); run<96, false, true>(); run<128, false, true>(); run<256, false, true>();
   return 0;
 }
