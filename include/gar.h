@@ -28,7 +28,7 @@
  *  - Stateless and re-entrant; concurrent calls need separate workspaces.
  *  - Results are bitwise deterministic for fixed inputs.
  *
- * Numerics (DESIGN.md §3 readings R1-R11): order statistics on canonical
+ * Numerics (DESIGN.md §3 readings R1-R14): order statistics on canonical
  * values (NaN -> +inf, -0 -> +0), averages as fp64 sums rounded once to fp32,
  * squared Euclidean distances from a tensor-core Gram matrix, ties to the
  * lower input index.
