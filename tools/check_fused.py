@@ -15,7 +15,7 @@ n, f, d = 31, 7, 5_000_011
 lo, hi = shard_bounds(d, rank, world)
 X = synth.make_gradients(n, f, hi - lo, seed=11 + rank, device=dev)
 bad = 0
-for rule in ("average", "median", "trimmed_mean", "krum", "multi_krum", "bulyan"):
+for rule in ("average", "median", "trimmed_mean", "krum", "multi_krum", "bulyan", "mda", "mean_around_median"):
     a = ShardedAggregator(rule, n, f, d, output="replicated", exchange="nccl").aggregate(X).clone()
     for mode, exch in (("replicated", "peer"), ("fused", "peer"), ("fused", "nccl"), ("fused-mc", "peer")):
         fu = ShardedAggregator(rule, n, f, d, output=mode, exchange=exch)
