@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/f1_pytest.log 2>&1; tail -2 gpurun_out/f1_pytest.log
+timeout 600 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/f1_smoke.log 2>&1; tail -1 gpurun_out/f1_smoke.log
+timeout 900 python bench.py > gpurun_out/f1_bench.log 2>&1; echo "bench rc=$?"
+timeout 600 python bench.py --impl reference > gpurun_out/f1_ref.log 2>&1; echo "ref rc=$?"
