@@ -86,6 +86,13 @@ cudaError_t launch_coord_bulyan_17_32(const CoordLaunch& L, cudaStream_t stream)
 cudaError_t launch_coord_bulyan_33_48(const CoordLaunch& L, cudaStream_t stream);
 cudaError_t launch_coord_bulyan_49_64(const CoordLaunch& L, cudaStream_t stream);
 cudaError_t launch_coord_bulyanb3(const CoordLaunch& L, cudaStream_t stream);
+cudaError_t launch_coord_average_ldg(const CoordLaunch& L, cudaStream_t stream);
+
+// A/B knob: GAR_AVG_RUNTIME_R=1 keeps the runtime-row-count direct-load Average
+static int getenv_flag_avg_runtime() {
+  static const int v = getenv("GAR_AVG_RUNTIME_R") != nullptr ? 1 : 0;
+  return v;
+}
 
 // beta = 3 Bulyan phase on the direct-load path (the default loader for Bulyan)
 static bool use_bulyan_b3(const CoordLaunch& L) {
@@ -99,6 +106,7 @@ cudaError_t launch_coord_select(int mode, const CoordLaunch& L, cudaStream_t str
   if (L.R < 1 || L.R > GAR_MAX_N) return cudaErrorInvalidValue;
   if (mode == kModeAverage) {
     if (L.R == 1) return launch_copy_row(L, stream);
+    if (L.R <= 8 && coord_loader_ldg(kModeAverage, L.R) && getenv_flag_avg_runtime() == 0) return launch_coord_average_ldg(L, stream);
     return launch_mode<kModeAverage, 0>(L, stream);
   }
   const int band = (L.R - 1) / 16;
