@@ -130,8 +130,11 @@ class Clocks:
                 pass
 
 
-def traffic_from_profiles(kernel_class):
-    """dram bytes per launch of the dominant kernel, from the committed ncu capture summary."""
+def traffic_from_profiles(kernel_class, workload, world):
+    """dram bytes per launch of the dominant kernel, from the committed ncu capture summary.
+    The capture is of the default single-GPU C3 step; other configurations report null."""
+    if workload != "C3" or world != 1:
+        return None
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as fh:
@@ -341,7 +344,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": kernels[dom]["frac"],
                      "algorithmic_bytes_per_launch": int(per_launch_bytes),
-                     "traffic": traffic_from_profiles(dom)},
+                     "traffic": traffic_from_profiles(dom, args.workload, world)},
         "kernels": kernels, "per_rule": per_rule, "clocks": clk.summary(),
         "stages_ms": stages, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
     }

@@ -85,20 +85,12 @@ cudaError_t launch_coord_bulyan_1_16(const CoordLaunch& L, cudaStream_t stream);
 cudaError_t launch_coord_bulyan_17_32(const CoordLaunch& L, cudaStream_t stream);
 cudaError_t launch_coord_bulyan_33_48(const CoordLaunch& L, cudaStream_t stream);
 cudaError_t launch_coord_bulyan_49_64(const CoordLaunch& L, cudaStream_t stream);
-cudaError_t launch_coord_bulyanb3(const CoordLaunch& L, cudaStream_t stream);
 cudaError_t launch_coord_average_ldg(const CoordLaunch& L, cudaStream_t stream);
 
 // A/B knob: GAR_AVG_RUNTIME_R=1 keeps the runtime-row-count direct-load Average
 static int getenv_flag_avg_runtime() {
   static const int v = getenv("GAR_AVG_RUNTIME_R") != nullptr ? 1 : 0;
   return v;
-}
-
-// beta = 3 Bulyan phase on the direct-load path (the default loader for Bulyan)
-static bool use_bulyan_b3(const CoordLaunch& L) {
-  if (L.R < 5 || L.R > 33 || L.R % 2 == 0 || L.f != (L.R - 3) / 2) return false;
-  static const bool off = getenv("GAR_BULYAN_B3_OFF") != nullptr;   // A/B knob
-  return !off && coord_loader_ldg(kModeBulyan, L.R) == 1;
 }
 
 cudaError_t launch_coord_select(int mode, const CoordLaunch& L, cudaStream_t stream) {
@@ -118,7 +110,6 @@ cudaError_t launch_coord_select(int mode, const CoordLaunch& L, cudaStream_t str
       switch (band) { case 0: return launch_coord_trimmed_1_16(L, stream); case 1: return launch_coord_trimmed_17_32(L, stream); case 2: return launch_coord_trimmed_33_48(L, stream); case 3: return launch_coord_trimmed_49_64(L, stream); }
       break;
     case kModeBulyan:
-      if (use_bulyan_b3(L)) return launch_coord_bulyanb3(L, stream);
       switch (band) { case 0: return launch_coord_bulyan_1_16(L, stream); case 1: return launch_coord_bulyan_17_32(L, stream); case 2: return launch_coord_bulyan_33_48(L, stream); case 3: return launch_coord_bulyan_49_64(L, stream); }
       break;
     default: break;

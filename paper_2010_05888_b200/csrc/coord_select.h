@@ -7,11 +7,7 @@
 
 namespace gar {
 
-// kModeBulyanB3: the Bulyan phase specialised to beta = 3 (f = (R-3)/2, R odd
-// >= 5; every BASELINE configuration), direct loads only.  A separate
-// instantiation keeps the general window path's registers and shared-memory
-// column out of the kernel.
-enum CoordMode { kModeAverage = 0, kModeMedian = 1, kModeTrimmed = 2, kModeBulyan = 3, kModeBulyanB3 = 4 };
+enum CoordMode { kModeAverage = 0, kModeMedian = 1, kModeTrimmed = 2, kModeBulyan = 3 };
 
 struct CoordLaunch {
   const float* const* rows;   // host array of n device row pointers

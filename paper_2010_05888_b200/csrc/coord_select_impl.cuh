@@ -396,22 +396,12 @@ __device__ __forceinline__ void coord_ldg_body(const CoordParams& p, const float
       res = static_cast<float>(s / R);
     } else {
       float v[N];
-      if constexpr (MODE == kModeBulyanB3) {
-        // row pointers re-read from shared memory each iteration (volatile):
-        // keeping N 64-bit pointers live costs 2N registers, and with them
-        // the kernel fits 5 CTAs per SM (tools/coord_exp.sh, r1_bulyan_b3.md)
 #pragma unroll
-        for (int r = 0; r < N; ++r) v[r] = __ldcs(*reinterpret_cast<const float* const volatile*>(&rowp[r]) + k);
-      } else {
-#pragma unroll
-        for (int r = 0; r < N; ++r) v[r] = __ldcs(rowp[r] + k);
-      }
+      for (int r = 0; r < N; ++r) v[r] = __ldcs(rowp[r] + k);
       if constexpr (MODE == kModeMedian) {
         res = median_column<N>(v);
       } else if constexpr (MODE == kModeTrimmed) {
         res = trimmed_column<N>(v, p.f);
-      } else if constexpr (MODE == kModeBulyanB3) {
-        res = bulyan_column_b3<N>(v, rowp, k);
       } else {
         float* col = reinterpret_cast<float*>(ldg_smem) + threadIdx.x;
         res = bulyan_dispatch<N>(v, col, kLdgThreads, p.f, rowp, k);
@@ -428,18 +418,6 @@ __global__ void __launch_bounds__(kLdgThreads) coord_ldg_kernel(const __grid_con
   coord_ldg_body<MODE, N>(p, rowp, sel_s);
 }
 
-// beta = 3 Bulyan phase: capped at 48 registers (5 CTAs per SM), no spills for
-// theta <= 33 (-Xptxas -v)
-#ifndef GAR_B3_MINB
-#define GAR_B3_MINB 5
-#endif
-template <int N>
-__global__ void __launch_bounds__(kLdgThreads, GAR_B3_MINB) coord_ldg_b3_kernel(const __grid_constant__ CoordParams p) {
-  __shared__ const float* rowp[GAR_MAX_N];
-  __shared__ int sel_s[GAR_MAX_N];
-  coord_ldg_body<kModeBulyanB3, N>(p, rowp, sel_s);
-}
-
 template <int MODE, int N>
 inline cudaError_t launch_ldg(const CoordLaunch& L, cudaStream_t stream) {
   CoordParams p;
@@ -454,12 +432,7 @@ inline cudaError_t launch_ldg(const CoordLaunch& L, cudaStream_t stream) {
   p.l2_hint = 0;
   p.num_tiles = 0;
   const size_t smem = (MODE == kModeBulyan) ? size_t(L.R) * kLdgThreads * sizeof(float) : 0;
-  void (*kern)(const CoordParams);
-  if constexpr (MODE == kModeBulyanB3) {
-    kern = coord_ldg_b3_kernel<N>;
-  } else {
-    kern = coord_ldg_kernel<MODE, N>;
-  }
+  auto kern = coord_ldg_kernel<MODE, N>;
   int occ = 0;
   cudaError_t e = cached_occupancy(kern, kLdgThreads, smem, &occ);
   if (e != cudaSuccess) return e;
@@ -516,17 +489,6 @@ inline cudaError_t launch_mode(const CoordLaunch& L, cudaStream_t stream) {
   } else {
     if (L.R <= 32) return launch_mode_w<MODE, 0, 15>(L, stream);
     return launch_mode_w<MODE, 0, 7>(L, stream);
-  }
-}
-
-// kModeBulyanB3 over odd R in [LO, HI] (LO odd)
-template <int LO, int HI>
-inline cudaError_t dispatch_b3(const CoordLaunch& L, cudaStream_t stream) {
-  if constexpr (LO > HI) {
-    return cudaErrorInvalidValue;
-  } else {
-    if (L.R == LO) return launch_ldg<kModeBulyanB3, LO>(L, stream);
-    return dispatch_b3<LO + 2, HI>(L, stream);
   }
 }
 

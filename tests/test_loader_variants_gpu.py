@@ -1,6 +1,8 @@
 """Both loaders of the coordinate-selection kernel (TMA bulk ring and direct
 LDG) are exercised whatever the default policy picks: each
-runs in a subprocess with GAR_COORD_LOADER forced, checked against the oracle."""
+runs in a subprocess with GAR_COORD_LOADER forced, checked against the oracle.
+The third case also turns off the compile-time-R Average for n <= 8, so the
+general direct-load Average it replaces stays parity-tested."""
 import os
 import subprocess
 import sys
@@ -35,11 +37,13 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("loader", ["tma", "ldg"])
+@pytest.mark.parametrize("loader", ["tma", "ldg", "ldg-general"])
 def test_loader_forced(loader):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    env = dict(os.environ, GAR_COORD_LOADER=loader)
+    env = dict(os.environ, GAR_COORD_LOADER=loader.split("-")[0])
+    if loader == "ldg-general":
+        env.update(GAR_AVG_RUNTIME_R="1")
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
