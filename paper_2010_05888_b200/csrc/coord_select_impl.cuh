@@ -379,6 +379,43 @@ __device__ __forceinline__ void coord_ldg_body(const CoordParams& p, const float
   __syncthreads();
   const int64_t d = p.d;
   const int64_t step = int64_t(gridDim.x) * kLdgThreads;
+#ifndef GAR_LDG_PREFETCH_MAX_N
+#define GAR_LDG_PREFETCH_MAX_N 47
+#endif
+  if constexpr (MODE != kModeAverage && N > 0 && N <= GAR_LDG_PREFETCH_MAX_N) {
+    // software pipeline: the next column's N loads are in flight while this
+    // column goes through the network.  Up to 47 rows the kernel stays within
+    // 128 registers (2+ CTAs per SM); measured 1-7 % faster for n = 11..47
+    // and 5-6 % slower at n = 63 (171 registers), profiles/r1_sweep_C5.md
+    int64_t k = int64_t(blockIdx.x) * kLdgThreads + threadIdx.x;
+    float v[N];
+    if (k < d) {
+#pragma unroll
+      for (int r = 0; r < N; ++r) v[r] = __ldcs(rowp[r] + k);
+    }
+    for (; k < d; k += step) {
+      const int64_t kn = k + step;
+      float vn[N];
+      if (kn < d) {
+#pragma unroll
+        for (int r = 0; r < N; ++r) vn[r] = __ldcs(rowp[r] + kn);
+      }
+      const float pv = p.extra.sgd ? __ldcs(p.out + k) : 0.0f;
+      float res;
+      if constexpr (MODE == kModeMedian) {
+        res = median_column<N>(v);
+      } else if constexpr (MODE == kModeTrimmed) {
+        res = trimmed_column<N>(v, p.f);
+      } else {
+        float* col = reinterpret_cast<float*>(ldg_smem) + threadIdx.x;
+        res = bulyan_dispatch<N>(v, col, kLdgThreads, p.f, rowp, k);
+      }
+      store_result(p.out, p.extra, k, res, pv);
+#pragma unroll
+      for (int r = 0; r < N; ++r) v[r] = vn[r];
+    }
+    return;
+  }
   for (int64_t k = int64_t(blockIdx.x) * kLdgThreads + threadIdx.x; k < d; k += step) {
     const float pv = p.extra.sgd ? __ldcs(p.out + k) : 0.0f;     // fused server step (see above)
     float res;
