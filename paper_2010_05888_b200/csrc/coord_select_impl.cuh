@@ -386,20 +386,10 @@ __device__ __forceinline__ void coord_ldg_body(const CoordParams& p, const float
     // software pipeline: the next column's N loads are in flight while this
     // column goes through the network.  Up to 47 rows the kernel stays within
     // 128 registers (2+ CTAs per SM); measured 1-7 % faster for n = 11..47
-    // and 5-6 % slower at n = 63 (171 registers), profiles/r1_sweep_C5.md
-    int64_t k = int64_t(blockIdx.x) * kLdgThreads + threadIdx.x;
-    float v[N];
-    if (k < d) {
-#pragma unroll
-      for (int r = 0; r < N; ++r) v[r] = __ldcs(rowp[r] + k);
-    }
-    for (; k < d; k += step) {
-      const int64_t kn = k + step;
-      float vn[N];
-      if (kn < d) {
-#pragma unroll
-        for (int r = 0; r < N; ++r) vn[r] = __ldcs(rowp[r] + kn);
-      }
+    // and 5-6 % slower at n = 63 (171 registers), profiles/r1_sweep_C5.md.
+    // Two register sets used alternately instead of the copy: more registers,
+    // measured slower at every n.
+    auto column = [&](float* v, int64_t k) {
       const float pv = p.extra.sgd ? __ldcs(p.out + k) : 0.0f;
       float res;
       if constexpr (MODE == kModeMedian) {
@@ -411,6 +401,19 @@ __device__ __forceinline__ void coord_ldg_body(const CoordParams& p, const float
         res = bulyan_dispatch<N>(v, col, kLdgThreads, p.f, rowp, k);
       }
       store_result(p.out, p.extra, k, res, pv);
+    };
+    auto load = [&](float* v, int64_t k) {
+#pragma unroll
+      for (int r = 0; r < N; ++r) v[r] = __ldcs(rowp[r] + k);
+    };
+    int64_t k = int64_t(blockIdx.x) * kLdgThreads + threadIdx.x;
+    float v[N];
+    if (k < d) load(v, k);
+    for (; k < d; k += step) {
+      const int64_t kn = k + step;
+      float vn[N];
+      if (kn < d) load(vn, kn);
+      column(v, k);
 #pragma unroll
       for (int r = 0; r < N; ++r) v[r] = vn[r];
     }
