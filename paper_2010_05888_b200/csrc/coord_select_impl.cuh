@@ -31,8 +31,12 @@ namespace gar {
 // 31 rows x 1 KB go 1.3 -> 5.5 TB/s from 1 to 8 issuing warps), so producer
 // warp p issues rows r = p mod kProducers and arms its own stage barrier.
 constexpr int kProducers = 4;
-template <int N>
-constexpr int consumer_warps() { return N <= 32 ? 15 : 7; }
+// Consumer warps per CTA (one CTA per SM).  The trimmed mean is ALU-bound
+// (FMNMX network) and gains from more warps to overlap: 24 warps (2 stages of
+// 95 KB at 31 rows) run C3 in 0.62 ms against 0.69 with 15; the Median, at
+// HBM speed, is best with 15 (3 stages).  Measured in profiles/r1_loader_choice.md.
+template <int MODE, int N>
+constexpr int consumer_warps() { return N > 32 ? 7 : (MODE == kModeTrimmed ? 24 : 15); }
 
 struct CoordParams {
   RowPtrs rows;
@@ -525,7 +529,7 @@ template <int MODE, int N>
 inline cudaError_t launch_mode(const CoordLaunch& L, cudaStream_t stream) {
   if (coord_loader_ldg(MODE, L.R)) return launch_ldg<MODE, N>(L, stream);
   if constexpr (N > 0) {
-    return launch_mode_w<MODE, N, consumer_warps<N>()>(L, stream);
+    return launch_mode_w<MODE, N, consumer_warps<MODE, N>()>(L, stream);
   } else {
     if (L.R <= 32) return launch_mode_w<MODE, 0, 15>(L, stream);
     return launch_mode_w<MODE, 0, 7>(L, stream);
