@@ -31,14 +31,17 @@ namespace gar {
 // 31 rows x 1 KB go 1.3 -> 5.5 TB/s from 1 to 8 issuing warps), so producer
 // warp p issues rows r = p mod kProducers and arms its own stage barrier.
 constexpr int kProducers = 4;
-// Consumer warps per CTA (one CTA per SM).  The trimmed mean is ALU-bound
-// (FMNMX network) and gains from more warps to overlap: 24 warps (2 stages of
-// 95 KB at 31 rows) run C3 in 0.62 ms against 0.69 with 15; the Median, at
+// Consumer warps per CTA (one CTA per SM).  The trimmed mean and the Bulyan
+// phase are ALU-bound (FMNMX networks) and gain from more warps to overlap: 24
+// warps (2 stages of 95 KB at 31 rows) run the C3 trimmed mean in 0.62 ms
+// against 0.69 with 15, and C3 Bulyan in 0.99 against 1.035; the Median, at
 // HBM speed, is best with 15 (3 stages).  Above 32 rows 12 warps (2 stages of
 // <= 98 KB): the Median of 63 in 1.16 ms against 1.43 with 7 and 1.40 with
 // direct loads.  Measured in profiles/r1_loader_choice.md.
 template <int MODE, int N>
-constexpr int consumer_warps() { return N > 32 ? 12 : (MODE == kModeTrimmed ? 24 : 15); }
+constexpr int consumer_warps() {
+  return N > 32 ? 12 : ((MODE == kModeTrimmed || MODE == kModeBulyan) ? 24 : 15);
+}
 
 struct CoordParams {
   RowPtrs rows;
