@@ -492,11 +492,10 @@ inline cudaError_t launch_ldg(const CoordLaunch& L, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-// Loader selection (measured on B200, tools/ab_step.py): with 4 issuing warps the
-// TMA ring wins up to 32 rows (C3: Average 0.47 ms vs 0.53, Median 0.52 vs
-// 0.65); direct loads win for the Bulyan phase (its sort-and-window consumer is
-// the bottleneck) and above 32 rows (the ring only fits 896 B copies).
-// GAR_COORD_LOADER=tma|ldg forces one.
+// Loader selection (measured on B200, tools/ab_step.py, profiles/r1_loader_choice.md):
+// the TMA ring (4 issuing warps) for the Median at every row count, for averages
+// and the trimmed mean at 17..32 and 48..64 rows, for the Bulyan phase at
+// 17..32 rows; direct loads elsewhere.  GAR_COORD_LOADER=tma|ldg forces one.
 // Returns 1 for LDG.
 int coord_loader_ldg(int mode, int R);
 
