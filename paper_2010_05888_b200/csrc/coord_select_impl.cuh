@@ -494,8 +494,8 @@ inline cudaError_t launch_ldg(const CoordLaunch& L, cudaStream_t stream) {
 
 // Loader selection (measured on B200, tools/ab_step.py, profiles/r1_loader_choice.md):
 // the TMA ring (4 issuing warps) for the Median at every row count, for averages
-// and the trimmed mean at 17..32 and 48..64 rows, for the Bulyan phase at
-// 17..32 rows; direct loads elsewhere.  GAR_COORD_LOADER=tma|ldg forces one.
+// at 17..32 and 48..64 rows, the trimmed mean at 13..32 and 48..64 rows, the
+// Bulyan phase at 17..32 rows; direct loads elsewhere.  GAR_COORD_LOADER=tma|ldg forces one.
 // Returns 1 for LDG.
 int coord_loader_ldg(int mode, int R);
 
