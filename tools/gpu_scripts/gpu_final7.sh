@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/f7_pytest.log 2>&1; tail -2 gpurun_out/f7_pytest.log
+timeout 600 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/f7_smoke.log 2>&1; tail -1 gpurun_out/f7_smoke.log
+timeout 900 python tools/sweep.py > gpurun_out/f7_sweep.md 2>&1; echo "sweep rc=$?"
+timeout 900 python bench.py > gpurun_out/f7_bench.log 2>&1; echo "bench rc=$?"; grep '^{' gpurun_out/f7_bench.log | tail -1 | cut -c1-300
