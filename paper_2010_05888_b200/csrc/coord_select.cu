@@ -53,13 +53,12 @@ int coord_loader_ldg(int mode, int R) {
   if (forced >= 0) return forced;
   // Measured per mode on B200 across n = 7..63 (profiles/r1_loader_choice.md):
   // the TMA ring wins for the Median at every row count, for averages at 17..32
-  // and 48..64 rows, for the trimmed mean (24 consumer warps) at 13..32 and
-  // 48..64 rows, and for the Bulyan phase (24 consumer warps) at 17..32 rows;
-  // direct loads win elsewhere.
+  // and 48..64 rows, for the trimmed mean above 12 rows, and for the Bulyan
+  // phase (24 consumer warps) at 17..32 rows; direct loads win elsewhere.
   switch (mode) {
     case kModeMedian: return 0;
     case kModeAverage: return ((R > 16 && R <= 32) || R >= 48) ? 0 : 1;
-    case kModeTrimmed: return ((R > 12 && R <= 32) || R >= 48) ? 0 : 1;
+    case kModeTrimmed: return R > 12 ? 0 : 1;
     case kModeBulyan: return (R > 16 && R <= 32) ? 0 : 1;
     default: return 1;
   }

@@ -37,10 +37,13 @@ constexpr int kProducers = 4;
 // against 0.69 with 15, and C3 Bulyan in 0.99 against 1.035; the Median, at
 // HBM speed, is best with 15 (3 stages).  Above 32 rows 12 warps (2 stages of
 // <= 98 KB): the Median of 63 in 1.16 ms against 1.43 with 7 and 1.40 with
-// direct loads.  Measured in profiles/r1_loader_choice.md.
+// direct loads; the trimmed mean takes 16 at 33..48 rows (n = 39: 0.85 ms
+// against 0.93 with direct loads).  Measured in profiles/r1_loader_choice.md.
 template <int MODE, int N>
 constexpr int consumer_warps() {
-  return N > 32 ? 12 : ((MODE == kModeTrimmed || MODE == kModeBulyan) ? 24 : 15);
+  if constexpr (N > 48) return 12;
+  if constexpr (N > 32) return MODE == kModeTrimmed ? 16 : 12;
+  return (MODE == kModeTrimmed || MODE == kModeBulyan) ? 24 : 15;
 }
 
 struct CoordParams {
@@ -494,8 +497,8 @@ inline cudaError_t launch_ldg(const CoordLaunch& L, cudaStream_t stream) {
 
 // Loader selection (measured on B200, tools/ab_step.py, profiles/r1_loader_choice.md):
 // the TMA ring (4 issuing warps) for the Median at every row count, for averages
-// at 17..32 and 48..64 rows, the trimmed mean at 13..32 and 48..64 rows, the
-// Bulyan phase at 17..32 rows; direct loads elsewhere.  GAR_COORD_LOADER=tma|ldg forces one.
+// at 17..32 and 48..64 rows, the trimmed mean above 12 rows, the Bulyan phase
+// at 17..32 rows; direct loads elsewhere.  GAR_COORD_LOADER=tma|ldg forces one.
 // Returns 1 for LDG.
 int coord_loader_ldg(int mode, int R);
 
