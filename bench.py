@@ -148,7 +148,11 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    import paper_2010_05888_b200 as gar
+    import __graft_entry__
+    # compile libgar.so in-tree if missing or stale (clean checkout), outside
+    # any timed region; concurrent ranks serialise on the builder's lock
+    __graft_entry__.ensure_built(with_oracle=False)
+    import paper_2010_05888_b200 as gar  # noqa: F401
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -2,8 +2,10 @@
 
 Every function here has the name of the C entry point it wraps and takes
 torch tensors (device memory) where the C call takes device pointers.  No
-step of the method runs in Python; there is no CPU fallback: if libgar.so is
-missing or was built without the kernels, importing this module raises.
+step of the method runs in Python; there is no CPU fallback: the library is
+loaded on the first C call, and if libgar.so is missing or was built without
+the kernels that call raises ImportError.  (Loading lazily lets the package --
+and its builder -- be imported on a clean checkout before anything is built.)
 """
 from __future__ import annotations
 
@@ -70,7 +72,22 @@ def _load():
     return L
 
 
-lib = _load()
+class _LazyLib:
+    """libgar.so, loaded (and its signatures declared) on first attribute access."""
+
+    _cdll = None
+
+    def __getattr__(self, name):
+        if _LazyLib._cdll is None:
+            _LazyLib._cdll = _load()
+        return getattr(_LazyLib._cdll, name)
+
+    @staticmethod
+    def loaded() -> bool:
+        return _LazyLib._cdll is not None
+
+
+lib = _LazyLib()
 
 
 def header_functions() -> list[str]:

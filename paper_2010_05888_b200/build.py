@@ -1,11 +1,18 @@
 """Build libgar.so (sm_100a) in-tree: nvcc -gencode arch=compute_100a,code=sm_100a.
 
 Objects go to ``_build/``; units are compiled in parallel and only rebuilt
-when their source or any header is newer.  ``python -m paper_2010_05888_b200.build``.
+when their source or any header is newer.  This file imports nothing from the
+package, so it can run on a clean checkout before libgar.so exists:
+
+    python paper_2010_05888_b200/build.py        (or python -m paper_2010_05888_b200.build)
+
+Concurrent builders (one per torchrun rank) serialise on ``_build/.lock``; the
+later ones find everything up to date.
 """
 from __future__ import annotations
 
 import concurrent.futures as cf
+import fcntl
 import glob
 import os
 import subprocess
@@ -47,8 +54,17 @@ def _compile(src, obj, log):
 
 
 def build(verbose: bool = False, jobs: int | None = None) -> str:
-    _regen_networks()
     os.makedirs(OBJ, exist_ok=True)
+    with open(os.path.join(OBJ, ".lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            return _build_locked(verbose, jobs)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
+
+
+def _build_locked(verbose: bool, jobs: int | None) -> str:
+    _regen_networks()
     hdr_mtime = max(os.path.getmtime(h) for h in _headers())
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     todo, objs = [], []

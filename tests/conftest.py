@@ -30,10 +30,8 @@ def _ensure_built():
     are available both here and on the GPU box)."""
     # a failed build must fail the session: a stale libgar.so would silently
     # test old kernels
-    from paper_2010_05888_b200 import build as b
-    b.build()
-    import oracle
-    oracle.build()
+    import __graft_entry__
+    __graft_entry__.ensure_built()
 
 
 _ensure_built()
