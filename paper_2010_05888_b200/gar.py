@@ -152,17 +152,19 @@ def _select_rows(grads, idx):
     return [grads[i] for i in idx]
 
 
-def aggregate_sanitized(agg: "Aggregator", grads, out: torch.Tensor | None = None, d: int | None = None):
+def aggregate_sanitized(agg: "Aggregator", grads, out: torch.Tensor | None = None, d: int | None = None,
+                        indices: torch.Tensor | None = None):
     """SPEC's AggregationOutcome path: drop the non-finite inputs (they count
     toward f: the rule runs on n - e inputs with f - e), aggregate the rest.
-    Returns (out, excluded indices)."""
+    Returns (out, excluded indices).  indices (optional, Krum family / MDA):
+    receives the selection, numbered among the kept inputs."""
     kept, excluded = sanitize(grads, agg.f, d)
     if not excluded:
-        return agg.aggregate(grads, out=out, d=d), excluded
+        return agg.aggregate(grads, out=out, d=d, indices=indices), excluded
     e = len(excluded)
     sub = Aggregator(agg.rule, agg.n - e, agg.f - e, (agg.m or None) if agg.rule == "multi_krum" else None)
-    return sub.aggregate(_select_rows(grads, kept), out=out, d=d if d is not None else _lib.row_pointers(grads)[2]), \
-        excluded
+    dd = d if d is not None else _lib.row_pointers(grads)[2]
+    return sub.aggregate(_select_rows(grads, kept), out=out, d=dd, indices=indices), excluded
 
 
 def init(name: str, n: int, f: int, m: int | None = None) -> Aggregator:

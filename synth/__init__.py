@@ -12,7 +12,12 @@ Recipe:
 * Byzantine rows (f of them, at seeded positions), the paper's two attacks
   (§5.4 "random values" and "reversed vector x(-100)"):
   ceil(f/2) rows  -100 * (mu + sigma * z_b)  and  floor(f/2) rows  N(0, 1);
-* ``kind="clean"``: all n rows honest.
+* ``kind="clean"``: all n rows honest;
+* ``kind="separated"``: as "byzantine", but honest row spreads follow a seeded
+  permutation of the ladder sigma_j = sigma * 1.04^j, so every Krum score (and
+  every Bulyan round's best score) is separated from the next by far more than
+  the 1e-4 relative gap of SURVEY.md §8c-6: the selection is then well posed and
+  the GPU must reproduce it exactly (tests/gpu_helpers.py).
 
 Shapes follow PAPER.md Table 1 (l.481-498) and BASELINE.json ``configs``.
 """
@@ -73,7 +78,7 @@ def make_gradients(n: int, f: int, d: int, seed: int, kind: str = "byzantine",
     Rows are the n worker gradients; ``[:, :d]`` is the data.  Generated with a
     torch.Generator on ``device`` so large matrices never touch the host.
     """
-    if kind not in ("byzantine", "clean"):
+    if kind not in ("byzantine", "clean", "separated"):
         raise ValueError(kind)
     ld = aligned_ld(d) if ld is None else ld
     dev = torch.device(device)
@@ -81,7 +86,11 @@ def make_gradients(n: int, f: int, d: int, seed: int, kind: str = "byzantine",
     g.manual_seed(seed)
     x = torch.zeros((n, ld), dtype=torch.float32, device=dev)
     mu = torch.randn(d, generator=g, device=dev, dtype=torch.float32).mul_(0.01)
-    byz = set(byzantine_positions(n, f, seed).tolist()) if kind == "byzantine" else set()
+    byz = set(byzantine_positions(n, f, seed).tolist()) if kind != "clean" else set()
+    ladder = None
+    if kind == "separated":
+        rank = np.random.default_rng(seed ^ 0x1ADD).permutation(n)
+        ladder = [float(1.04 ** int(r)) for r in rank]
     n_rev = math.ceil(len(byz) / 2)
     byz_sorted = sorted(byz)
     reversed_rows = set(byz_sorted[:n_rev])
@@ -91,7 +100,7 @@ def make_gradients(n: int, f: int, d: int, seed: int, kind: str = "byzantine",
             row.copy_(torch.randn(d, generator=g, device=dev, dtype=torch.float32))
         else:
             torch.randn(d, generator=g, device=dev, dtype=torch.float32, out=row)
-            row.mul_(0.01).add_(mu)
+            row.mul_(0.01 if ladder is None else 0.01 * ladder[i]).add_(mu)
             if i in reversed_rows:
                 row.mul_(-100.0)
     return x

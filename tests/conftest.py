@@ -35,3 +35,12 @@ def _ensure_built():
 
 
 _ensure_built()
+
+
+def pytest_terminal_summary(terminalreporter):
+    """Selection-parity verdicts of the GPU tests (tests/gpu_helpers.py)."""
+    import sys as _s
+    h = _s.modules.get("gpu_helpers")
+    if h is not None and h.VERDICTS:
+        terminalreporter.write_line(f"selection verdicts: {dict(sorted(h.VERDICTS.items()))} "
+                                    f"(eps-tie only where the oracle's decision gap < {h.SEPARATED})")

@@ -8,6 +8,9 @@ import oracle
 
 KRUM_FAMILY = ("krum", "multi_krum", "bulyan")
 EPS_TIE = 1e-5          # selection-parity rule: relative score slack
+SEPARATED = 1e-4        # oracle score gaps above this make a decision well posed
+# selection verdicts of this session ({verdict: count}); printed by conftest at the end
+VERDICTS: dict = {}
 
 
 def to_device(x: np.ndarray) -> torch.Tensor:
@@ -62,6 +65,51 @@ def check_selection(rule, D_oracle: np.ndarray, f: int, m: int, sel_gpu: np.ndar
         assert abs(s[pick] - s[order[t]]) <= EPS_TIE * abs(s[order[t]]) + 1e-300, \
             f"{rule} position {t}: gpu {pick} ({s[pick]!r}) vs oracle {order[t]} ({s[order[t]]!r})"
     return "eps-tie"
+
+
+def decision_gap(rule, D_oracle: np.ndarray, f: int, m: int) -> float:
+    """The smallest relative score gap over the oracle's selection decisions:
+    Multi-Krum: between consecutive sorted scores at positions 0..m (the m
+    picks and the first rejected); Bulyan: per round, between the best and
+    second-best score of the pool.  Rounds with zero neighbours (every score
+    exactly 0 on both sides; the index rule decides) are exact by definition
+    and skipped.  Above SEPARATED, anything but an exact GPU selection is a bug."""
+    n = D_oracle.shape[0]
+    gap = np.inf
+    if rule == "bulyan":
+        pool = np.ones(n, np.uint8)
+        for _ in range(n - 2 * f):
+            members = np.flatnonzero(pool)
+            s = oracle.bulyan_round_scores(D_oracle, f, pool)
+            ss = sorted((s[i], i) for i in members)
+            if len(members) - f - 2 > 0 and len(ss) > 1:
+                gap = min(gap, (ss[1][0] - ss[0][0]) / max(abs(ss[1][0]), 1e-300))
+            pool[ss[0][1]] = 0
+        return gap
+    s = oracle.krum_scores(D_oracle, f)
+    if n - f - 2 <= 0:
+        return gap
+    o = sorted(range(n), key=lambda i: (s[i], i))
+    for t in range(min(m, n - 1)):
+        gap = min(gap, (s[o[t + 1]] - s[o[t]]) / max(abs(s[o[t + 1]]), 1e-300))
+    return gap
+
+
+def assert_selection(rule, D_oracle: np.ndarray, f: int, m: int, sel_gpu: np.ndarray,
+                     require_separated: bool = False) -> str:
+    """The strict selection check: the GPU selection must
+    be exactly the oracle's whenever the oracle's decisions are separated by
+    more than SEPARATED; an eps-tie verdict is accepted only for inputs whose
+    decision gap is below that (and tallied).  require_separated: the input
+    claims to be well separated (synth kind="separated"); assert that too."""
+    gap = decision_gap(rule, D_oracle, f, m)
+    if require_separated:
+        assert gap > SEPARATED, f"{rule}: input not well separated (gap {gap:.3e})"
+    verdict = check_selection(rule, D_oracle, f, m, sel_gpu)
+    if gap > SEPARATED:
+        assert verdict == "exact", f"{rule}: well-separated selection (gap {gap:.3e}) not exact: {list(sel_gpu)}"
+    VERDICTS[verdict] = VERDICTS.get(verdict, 0) + 1
+    return verdict
 
 
 def distances_close(D_gpu: np.ndarray, D_ref: np.ndarray, rtol: float = 1e-5):

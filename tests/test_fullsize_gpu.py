@@ -14,7 +14,7 @@ import torch
 
 import oracle
 import synth
-from gpu_helpers import KRUM_FAMILY, assert_same_bits, check_selection, distances_close
+from gpu_helpers import KRUM_FAMILY, assert_same_bits, assert_selection, distances_close
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -57,11 +57,42 @@ def test_c3_full_size(gar, c3, rule):
     if rule in KRUM_FAMILY:
         sel = idx[: agg.num_selected].cpu().numpy()
         mm = 1 if rule == "krum" else n - f - 2
-        check_selection(rule, D, f, mm, sel)
+        assert_selection(rule, D, f, mm, sel)
         ref = oracle.bulyan_coordinate_phase(xs, f, sel) if rule == "bulyan" else oracle.mean_of_rows(xs, sel)
     else:
         ref, _ = oracle.aggregate(rule, xs, f)
     assert_same_bits(got, ref, rule)
+
+
+@pytest.fixture(scope="module")
+def c3_separated(gar):
+    cfg = synth.CONFIGS["C3"]
+    X = synth.make_gradients(cfg.n, cfg.f, cfg.d, seed=synth.BASE_SEED + 12, device="cuda", kind="separated")
+    x = X[:, : cfg.d].cpu().numpy()
+    D = oracle.distances(x)
+    yield cfg, X, x, D
+    del X
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("rule", KRUM_FAMILY)
+def test_c3_full_size_separated_selection_exact(gar, c3_separated, rule):
+    """At the full C3 size, in the launch configuration bench.py times, on an
+    input whose oracle decisions are all separated by > 1e-4:
+    the selected indices equal the oracle's exactly (distances over the whole
+    25.6M-coordinate vectors), and the combine is bit-exact on a sample."""
+    cfg, X, x, D = c3_separated
+    n, f, d = cfg.n, cfg.f, cfg.d
+    agg = gar.init(rule, n, f)
+    idx = torch.full((64,), -1, dtype=torch.int32, device="cuda")
+    out = agg.aggregate(X, d=d, indices=idx)
+    torch.cuda.synchronize()
+    sel = idx[: agg.num_selected].cpu().numpy()
+    assert assert_selection(rule, D, f, 1 if rule == "krum" else n - f - 2, sel, require_separated=True) == "exact"
+    cols = sample_columns(d, 5)
+    xs = np.ascontiguousarray(x[:, cols])
+    ref = oracle.bulyan_coordinate_phase(xs, f, sel) if rule == "bulyan" else oracle.mean_of_rows(xs, sel)
+    assert_same_bits(out[torch.from_numpy(cols).cuda()].cpu().numpy(), ref, rule)
 
 
 def test_c3_distances_full_size(gar, c3):
@@ -92,7 +123,7 @@ def test_c4_full_size_median_and_krum(gar):
     idx = torch.full((64,), -1, dtype=torch.int32, device="cuda")
     out = agg.aggregate(X, d=d, indices=idx)
     sel = idx[:1].cpu().numpy()
-    check_selection("krum", D, f, 1, sel)
+    assert_selection("krum", D, f, 1, sel)
     assert_same_bits(out[tcols].cpu().numpy(), oracle.mean_of_rows(xs, sel), "krum C4")
     del X
     torch.cuda.empty_cache()

@@ -249,6 +249,39 @@ def test_krum_family_vs_brute():
     assert checked > 500
 
 
+def test_bulyan_round_scores_vs_brute():
+    """oracle_bulyan_round_scores (the eps-tie replay function of the selection
+    parity rule) against the brute-force subset minimum over
+    random pools R: score_i = min over (|R|-f-2)-subsets of R\\{i} of the summed
+    distances (reading R7), clamped at 0 neighbours; NaN
+    outside the pool.  A wrong pool, n instead of |R|, or a missing clamp fails."""
+    rng = np.random.default_rng(15)
+    checked = 0
+    for _ in range(300):
+        n = int(rng.integers(2, 10))
+        x = rng.standard_normal((n, int(rng.integers(1, 4)))).astype(np.float32)
+        D = oracle.distances(x)
+        for f in range(0, 3):
+            pool = (rng.random(n) < 0.7).astype(np.uint8)
+            if not pool.any():
+                pool[int(rng.integers(0, n))] = 1
+            members = [i for i in range(n) if pool[i]]
+            k = max(len(members) - f - 2, 0)
+            s = oracle.bulyan_round_scores(D, f, pool)
+            for i in range(n):
+                if not pool[i]:
+                    assert np.isnan(s[i])
+                    continue
+                want = brute.krum_score(D, i, members, k)
+                assert s[i] == pytest.approx(want, rel=1e-14, abs=0), (n, f, members, i)
+                checked += 1
+            # full pool: equals the Krum score table with n - f - 2 neighbours
+            if n >= 2 * f + 3:
+                np.testing.assert_allclose(oracle.bulyan_round_scores(D, f, np.ones(n, np.uint8)),
+                                           oracle.krum_scores(D, f), rtol=0, atol=0)
+    assert checked > 1000
+
+
 def test_bulyan_coordinate_phase_ties_vs_brute():
     """Integer-valued inputs make closeness ties (equal |y - med| on both sides)."""
     rng = np.random.default_rng(14)

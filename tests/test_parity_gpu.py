@@ -8,7 +8,7 @@ import torch
 
 import oracle
 import synth
-from gpu_helpers import (KRUM_FAMILY, assert_same_bits, check_selection, distances_close, to_device)
+from gpu_helpers import (KRUM_FAMILY, assert_same_bits, assert_selection, distances_close, to_device)
 
 pytestmark = pytest.mark.gpu
 
@@ -32,7 +32,8 @@ def run_rule(gar, rule, X, d, f, m=None):
     return out.cpu().numpy(), sel
 
 
-def check_rule(gar, rule, x, f, m=None, X=None):
+def check_rule(gar, rule, x, f, m=None, X=None, separated=False):
+    """separated: the input is synth kind="separated"; its selection must be exact."""
     n, d = x.shape
     X = to_device(x) if X is None else X
     out, sel = run_rule(gar, rule, X, d, f, m)
@@ -45,7 +46,7 @@ def check_rule(gar, rule, x, f, m=None, X=None):
     else:
         D = oracle.distances(x)
         mm = 1 if rule == "krum" else (n - f - 2 if m is None else m)
-        verdict = check_selection(rule, D, f, mm, sel)
+        verdict = assert_selection(rule, D, f, mm, sel, require_separated=separated)
         if rule == "bulyan":
             assert_same_bits(out, oracle.bulyan_coordinate_phase(x, f, sel), rule)
         else:
@@ -61,6 +62,23 @@ def check_rule(gar, rule, x, f, m=None, X=None):
 def test_recipe_parity(gar, rule, n, f, d):
     x = synth.make_gradients(n, f, d, seed=synth.BASE_SEED + n, ld=d).numpy()
     check_rule(gar, rule, x, f)
+
+
+@pytest.mark.parametrize("n,f,d", [(11, 2, synth.MNIST_CNN_D), (19, 4, 200_003), (31, 7, 300_001),
+                                   (7, 1, 4099), (63, 15, 40_005), (15, 3, 1), (64, 15, 3001), (47, 11, 3001),
+                                   (5, 0, 3001), (4, 0, 1000)])
+@pytest.mark.parametrize("rule", KRUM_FAMILY)
+def test_separated_selection_exact(gar, rule, n, f, d):
+    """Well-posed selections (every oracle decision gap > 1e-4, SURVEY.md
+    §8c-6; asserted on the input): the GPU indices must equal the oracle's
+    exactly, for Krum, Multi-Krum (default m and m = 3) and Bulyan (PAPER.md
+    l.210-212, l.219-221), and the combine must be bit-exact."""
+    if rule == "bulyan" and n < 4 * f + 3:
+        f = (n - 3) // 4
+    x = synth.make_gradients(n, f, d, seed=synth.BASE_SEED + 7 * n, ld=d, kind="separated").numpy()
+    assert check_rule(gar, rule, x, f, separated=True) == "exact"
+    if rule == "multi_krum" and n - f - 2 >= 3:
+        assert check_rule(gar, rule, x, f, m=3, separated=True) == "exact"
 
 
 @pytest.mark.parametrize("n", list(range(1, 65)))
@@ -293,24 +311,34 @@ def test_sanitize_and_aggregate(gar, rule):
     x[9, d - 1] = np.nan
     X = to_device(x)
     a = gar.init(rule, n, f)
-    out, excluded = gar.aggregate_sanitized(a, X, d=d)
+    idx = torch.full((64,), -1, dtype=torch.int32, device="cuda")
+    out, excluded = gar.aggregate_sanitized(a, X, d=d, indices=idx if rule != "median" and rule != "trimmed_mean"
+                                            else None)
     torch.cuda.synchronize()
     kept, bad = oracle.sanitize(x, f)
     assert excluded == bad == [4, 9]
-    xs, fs = x[kept], f - len(bad)
+    xs, fs = np.ascontiguousarray(x[kept]), f - len(bad)
+    got = out.cpu().numpy()
     if rule == "median":
-        ref = oracle.median(xs, fs)
+        assert_same_bits(got, oracle.median(xs, fs), rule)
     elif rule == "trimmed_mean":
-        ref = oracle.trimmed_mean(xs, fs)
-    elif rule == "multi_krum":
-        ref = oracle.multi_krum(xs, fs)[0]
-    elif rule == "bulyan":
-        ref = oracle.bulyan(xs, fs)[0]
+        assert_same_bits(got, oracle.trimmed_mean(xs, fs), rule)
     else:
-        ref = oracle.mda(xs, fs)[0]
-    np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-6, atol=1e-9)
-    if rule in ("median", "trimmed_mean"):
-        assert_same_bits(out.cpu().numpy(), ref, rule)
+        # selection (numbered among the kept rows) against the oracle, then a bit-exact combine
+        ns = len(kept)
+        D = oracle.distances(xs)
+        if rule == "mda":
+            sel = idx[: ns - fs].cpu().numpy()
+            assert sel.tolist() == oracle.mda_select(D, fs).tolist()
+            assert_same_bits(got, oracle.mean_of_rows(xs, sel), rule)
+        elif rule == "multi_krum":
+            sel = idx[: ns - fs - 2].cpu().numpy()
+            assert_selection(rule, D, fs, ns - fs - 2, sel)
+            assert_same_bits(got, oracle.mean_of_rows(xs, sel), rule)
+        else:
+            sel = idx[: ns - 2 * fs].cpu().numpy()
+            assert_selection(rule, D, fs, 0, sel)
+            assert_same_bits(got, oracle.bulyan_coordinate_phase(xs, fs, sel), rule)
 
 
 def test_binding_rejects_bad_buffers(gar):
@@ -409,7 +437,7 @@ def test_sharded_building_blocks_equal_whole(gar):
         sel_sh = idx[:k].cpu().numpy()
         D = oracle.distances(x)
         mm = 1 if rule == "krum" else n - f - 2
-        check_selection(rule, D, f, mm, sel_sh)
+        assert_selection(rule, D, f, mm, sel_sh)
         if sel_sh.tolist() == sel.tolist():
             assert_same_bits(out.cpu().numpy(), whole, rule)
 
