@@ -71,9 +71,12 @@ def decision_gap(rule, D_oracle: np.ndarray, f: int, m: int) -> float:
     """The smallest relative score gap over the oracle's selection decisions:
     Multi-Krum: between consecutive sorted scores at positions 0..m (the m
     picks and the first rejected); Bulyan: per round, between the best and
-    second-best score of the pool.  Rounds with zero neighbours (every score
-    exactly 0 on both sides; the index rule decides) are exact by definition
-    and skipped.  Above SEPARATED, anything but an exact GPU selection is a bug."""
+    second-best score of the pool.  Exact ties (bitwise-equal oracle scores:
+    rounds with zero neighbours, where every score is 0, or structurally equal
+    sums such as the shared nearest pair D_ij = D_ji with one neighbour) are
+    decided by the lower-index rule, not by a score difference, and are
+    skipped: the GPU must reproduce them too.  Above SEPARATED, anything but an
+    exact GPU selection is a bug."""
     n = D_oracle.shape[0]
     gap = np.inf
     if rule == "bulyan":
@@ -82,7 +85,7 @@ def decision_gap(rule, D_oracle: np.ndarray, f: int, m: int) -> float:
             members = np.flatnonzero(pool)
             s = oracle.bulyan_round_scores(D_oracle, f, pool)
             ss = sorted((s[i], i) for i in members)
-            if len(members) - f - 2 > 0 and len(ss) > 1:
+            if len(members) - f - 2 > 0 and len(ss) > 1 and ss[1][0] != ss[0][0]:
                 gap = min(gap, (ss[1][0] - ss[0][0]) / max(abs(ss[1][0]), 1e-300))
             pool[ss[0][1]] = 0
         return gap
@@ -91,7 +94,8 @@ def decision_gap(rule, D_oracle: np.ndarray, f: int, m: int) -> float:
         return gap
     o = sorted(range(n), key=lambda i: (s[i], i))
     for t in range(min(m, n - 1)):
-        gap = min(gap, (s[o[t + 1]] - s[o[t]]) / max(abs(s[o[t + 1]]), 1e-300))
+        if s[o[t + 1]] != s[o[t]]:
+            gap = min(gap, (s[o[t + 1]] - s[o[t]]) / max(abs(s[o[t + 1]]), 1e-300))
     return gap
 
 
