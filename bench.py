@@ -130,15 +130,18 @@ class Clocks:
                 pass
 
 
-def traffic_from_profiles(kernel_class, workload, world):
-    """dram bytes per launch of the dominant kernel, from the committed ncu capture summary.
-    The capture is of the default single-GPU C3 step; other configurations report null."""
+def traffic_from_profiles(kernel, workload, world):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`,
+    from the committed `ncu --set full` capture of the default single-GPU C3
+    step (profiles/traffic.json, written by tools/summarize_ncu.py); other
+    configurations report null."""
     if workload != "C3" or world != 1:
         return None
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(kernel_class)
+            t = json.load(fh)
+        return t.get("per_kernel", {}).get(kernel.split("<")[0])
     except Exception:
         return None
 
@@ -198,7 +201,7 @@ def run_ours(args):
 
             def mark(label, r=r, last=last):
                 e = ev()
-                segs.append((CLASS[label], r, last[0], e))
+                segs.append((label, r, last[0], e))
                 last[0] = e
             aggs[r].aggregate(X, out_local=outs[r], out_full=full[r], mark=mark, barrier=last_rule)
         for r in RULES:              # output="replicated-async": the step ends when every gather has
@@ -221,9 +224,9 @@ def run_ours(args):
     ms = t0.elapsed_time(t1)
     # per-segment device times
     cls_ms, rule_ms = {}, {r: 0.0 for r in RULES}
-    for cls, r, a, b in segs:
+    for lab, r, a, b in segs:
         t = a.elapsed_time(b)
-        cls_ms[cls] = cls_ms.get(cls, 0.0) + t
+        cls_ms[CLASS[lab]] = cls_ms.get(CLASS[lab], 0.0) + t
         rule_ms[r] += t
     if world > 1:
         t = torch.tensor([ms] + [rule_ms[r] for r in RULES], dtype=torch.float64, device=dev)
@@ -244,6 +247,9 @@ def run_ours(args):
         obuf = [outs, {r: torch.empty(dl, dtype=torch.float32, device=dev) for r in RULES}]
         fbuf = [full, {r: (torch.empty_like(full[r]) if full[r] is not None else None) for r in RULES}]
         h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        pub = {r: gar.init(r, n, f) for r in RULES}
+        for r in RULES:                            # workspace allocation outside the timed region
+            pub[r].aggregate(X, out=outs[r], d=dl)
         consumed = [None, None]                    # compute finished reading xbuf[b]
         drained = [None, None]                     # D2H finished reading obuf[b]
         rule_drained = {}
@@ -267,9 +273,12 @@ def run_ours(args):
             for r in RULES:
                 if r in rule_drained:              # fused outputs live in the aggregator's own buffer
                     stream.wait_event(rule_drained[r])
-                res = aggs[r].aggregate(xbuf[bb], out_local=obuf[bb][r], out_full=fbuf[bb][r],
-                                        barrier=r == RULES[-1])
-                aggs[r].wait()
+                if world == 1:         # the public single-GPU call: Aggregator.aggregate -> gar_aggregate_ex
+                    res = pub[r].aggregate(xbuf[bb], out=obuf[bb][r], d=dl)
+                else:                  # the public multi-GPU call (Aggregator.aggregate_sharded's engine)
+                    res = aggs[r].aggregate(xbuf[bb], out_local=obuf[bb][r], out_full=fbuf[bb][r],
+                                            barrier=r == RULES[-1])
+                    aggs[r].wait()
                 local_res = res[lo:hi] if res.numel() > dl else res
                 done = torch.cuda.Event()
                 done.record(stream)
@@ -295,9 +304,12 @@ def run_ours(args):
         e2e = {"value": round(len(RULES) * n * d * 4 / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": int(X.numel() * 4 * world),
                "d2h_bytes_per_step": int(len(RULES) * dl * 4 * world),
-               "path": "Aggregator.aggregate (gar_aggregate_ex) per rule; inputs H2D from pinned host and six "
-                       "results D2H every step, on copy streams, double-buffered so step k+1's H2D overlaps "
-                       "step k's aggregation"}
+               "path": ("paper_2010_05888_b200.init(rule, n, f).aggregate(X) per rule (one gar_aggregate_ex C call "
+                        "each)" if world == 1 else
+                        "dist.ShardedAggregator.aggregate per rule (gar_gram_exchange / gar_select_from_gram / "
+                        "gar_combine_bcast for the Krum family, gar_aggregate_bcast otherwise)")
+                       + "; inputs H2D from pinned host and six results D2H every step, on copy streams, "
+                         "double-buffered so step k+1's H2D overlaps step k's aggregation"}
 
     if rank != 0:
         if world > 1:
@@ -307,30 +319,53 @@ def run_ours(args):
     ms_step = ms / args.steps
     grad_bytes = len(RULES) * n * d * 4
     value = grad_bytes / (ms_step * 1e-3) / 1e9
-    # dominant kernel roofline (single-GPU algorithmic bytes per launch)
-    launches = {"coord_select": 6, "gram": 3}
-    bytes_cls = {
-        "coord_select": sum(rule_bytes(r, n, f, dl) for r in ("average", "median", "trimmed_mean"))
-        + sum(4 * dl * (R + 1) for R in (1, n - f - 2, n - 2 * f)),
-        "gram": 3 * 4 * n * dl,
-    }
+    # ---- per-kernel roofline: every timed segment is one
+    # libgar kernel launch, except "gram", which is the Gram kernel plus the
+    # deterministic n x n partial reduction (~1 % of it; counted against the
+    # Gram, so its fraction is conservative).  Algorithmic bytes per launch on
+    # this rank's slice: rows read + output written.
+    m_mk, theta = n - f - 2, n - 2 * f
+    np_ = 8 if n <= 8 else 16 if n <= 16 else 32 if n <= 32 else 64
+    kern = {}
+
+    def add(name, t_ms, nbytes):
+        k = kern.setdefault(name, {"ms_per_step": 0.0, "launches_per_step": 0, "bytes": 0})
+        k["ms_per_step"] += t_ms / args.steps
+        k["launches_per_step"] += 1
+        k["bytes"] += nbytes
+    seg_name = {"combine": {"krum": ("copy_row_kernel", 4 * dl * 2),
+                            "multi_krum": ("coord_select_kernel<average of m selected rows>", 4 * dl * (m_mk + 1)),
+                            "bulyan": ("coord_select_kernel<bulyan coordinate phase>", 4 * dl * (theta + 1))}}
+    for lab, r, a, b in segs:
+        t = a.elapsed_time(b)
+        if lab == "gram":
+            add(f"gram_tc_kernel<{np_}>", t, 4 * n * dl)
+        elif lab == "select":
+            add("select_kernel", t, 0)
+        elif lab == "combine":
+            add(*((seg_name["combine"][r][0], t, seg_name["combine"][r][1])))
+        elif lab == "coord":
+            add(f"coord_select_kernel<{r}>", t, 4 * dl * (n + 1))
+    reps = args.steps   # every segment was recorded once per rule per step
     kernels = {}
-    for c in ("coord_select", "gram"):
-        t = cls_ms.get(c, 0.0) / args.steps
-        ach = bytes_cls[c] / (t * 1e-3) / 1e9 if t > 0 else 0.0
-        kernels[c] = {"ms_per_step": round(t, 4), "launches_per_step": launches[c],
-                      "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 4),
-                      "share_of_step": round(t / ms_step, 4)}
+    for name, k in kern.items():
+        per_launch_ms = k["ms_per_step"] * reps / k["launches_per_step"]     # average launch duration
+        per_launch_bytes = k["bytes"] / k["launches_per_step"]
+        ach = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 and per_launch_bytes else 0.0
+        kernels[name] = {"ms_per_step": round(k["ms_per_step"], 4),
+                         "launches_per_step": k["launches_per_step"] // reps,
+                         "ms_per_launch": round(per_launch_ms, 4),
+                         "algorithmic_bytes_per_launch": int(per_launch_bytes),
+                         "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 4) if ach else None,
+                         "share_of_step": round(k["ms_per_step"] / ms_step, 4)}
+    dom = max((k for k in kernels if kernels[k]["algorithmic_bytes_per_launch"]),
+              key=lambda k: kernels[k]["ms_per_step"])
     # libgar kernels per step: 1 per coordinate-wise rule; per Krum-family rule
     # Gram partials + reduction + selection + combine, and with the peer-memory
     # exchange (N > 1) the reduction is a reduce-and-store plus a gather kernel
     peer = world > 1 and aggs["krum"]._use_peer_exchange(dev)
     launches_per_step = 3 + 3 * (5 if peer else 4)
-    # every stage class of the step (ms per step, rank 0): kernels plus the
-    # exchange / select / gather stages of the d-sharded path
     stages = {c: round(t / args.steps, 4) for c, t in sorted(cls_ms.items())}
-    dom = max(kernels, key=lambda c: kernels[c]["ms_per_step"])
-    per_launch_bytes = bytes_cls[dom] / launches[dom]
     per_rule = {}
     for r in RULES:
         t = rule_ms[r] / args.steps
@@ -347,7 +382,9 @@ def run_ours(args):
                    "l2": f"inputs {n * d * 4 / 1e9:.2f} GB > 126 MB L2 (no flush needed)"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": kernels[dom]["frac"],
-                     "algorithmic_bytes_per_launch": int(per_launch_bytes),
+                     "algorithmic_bytes_per_launch": kernels[dom]["algorithmic_bytes_per_launch"],
+                     "launches_per_step": kernels[dom]["launches_per_step"],
+                     "share_of_step": kernels[dom]["share_of_step"],
                      "traffic": traffic_from_profiles(dom, args.workload, world)},
         "kernels": kernels, "per_rule": per_rule, "clocks": clk.summary(),
         "stages_ms": stages, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
@@ -406,7 +443,8 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg.name}: n={cfg.n} f={cfg.f} d={cfg.d}, GARs {'/'.join(RULES)}",
-                       "n": cfg.n, "f": cfg.f, "d": cfg.d},
+                       "n": cfg.n, "f": cfg.f, "d": cfg.d,
+                       "sample": f"each step aggregates the {part} (value = gradient bytes of the sample / time)"},
             "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": oracle.default_threads(),
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

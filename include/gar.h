@@ -88,6 +88,14 @@ size_t gar_workspace_bytes(gar_rule rule, int n, int f, int64_t d);
  * invalid arguments.  Pure host function. */
 int gar_num_selected(gar_rule rule, int n, int f, int m);
 
+/* The argument checks every entry point runs first, as a pure host function
+ * (no CUDA call): GAR_OK, GAR_ERR_INVALID_ARGUMENT (unknown rule, n outside
+ * [1, 64], f < 0), GAR_ERR_QUORUM (n below the rule's bound: PAPER.md l.208,
+ * l.212, l.225), GAR_ERR_INVALID_M (Multi-Krum m outside [1, n-f-2], l.210)
+ * or GAR_ERR_UNSUPPORTED (MDA with more than 2^31 candidate subsets C(n, f)).
+ * Lets a binding report the real reason where gar_num_selected returns 0. */
+gar_status gar_check_args(gar_rule rule, int n, int f, int m);
+
 /* out = GAR_rule(grads[0..n)) over d coordinates (default m = n-f-2 for
  * Multi-Krum).  Allocates its workspace with cudaMallocAsync on `stream`. */
 gar_status gar_aggregate(gar_rule rule, const float* const* grads, int n, int f, int64_t d,
@@ -211,8 +219,10 @@ gar_status gar_combine_sgd(gar_rule rule, const float* const* grads, int n, int 
  * peer_flags: host array [world] of every rank's flag array (uint32[world],
  *   zero before the first call, 4-byte aligned).
  * epoch: > the previous call's epoch, the same on every rank for one call.
- * world <= 8.  A rank that does not arrive within ~10 s yields NaN in
- * gram_dev instead of a hang.  workspace as for gar_gram_partial.
+ * world <= 8.  A rank that does not arrive within ~10 s makes the kernel
+ * trap instead of hanging: the stream's context then holds a sticky launch
+ * error, which this or the next call (or a stream synchronize) reports
+ * (GAR_ERR_CUDA); no result is produced.  workspace as for gar_gram_partial.
  * stage_rows (optional, host array of n DEVICE fp32[d_local] buffers,
  * 16-byte aligned): the Gram kernel also writes every row's slice there from
  * its staging ring (bulk stores), so rows read from other GPUs' memory

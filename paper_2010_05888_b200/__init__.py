@@ -10,7 +10,7 @@ this package only marshals arguments.
     idx = g.select(list_of_cuda_fp32_tensors)         # int32 indices (Krum family)
 """
 from ._lib import (GarError, RULES, gar_aggregate, gar_aggregate_ex, gar_combine, gar_distances,  # noqa: F401
-                   gar_gram_partial, gar_num_selected, gar_select, gar_select_from_gram, gar_status_string,
+                   gar_gram_partial, gar_num_selected, gar_check_args, gar_select, gar_select_from_gram, gar_status_string,
                    gar_last_error, gar_gram_exchange,
                    gar_aggregate_bcast, gar_combine_bcast, gar_aggregate_mcast, gar_combine_mcast,
                    gar_trimmed_membership, gar_aggregate_sgd, gar_combine_sgd, gar_nonfinite_rows,
@@ -19,6 +19,6 @@ from .gar import Aggregator, TooManyNonFinite, aggregate_sanitized, init, saniti
 
 __all__ = ["init", "Aggregator", "GarError", "RULES", "gar_aggregate", "gar_aggregate_ex", "gar_select",
            "gar_distances", "gar_gram_partial", "gar_select_from_gram", "gar_combine", "gar_workspace_bytes",
-           "gar_num_selected", "gar_status_string", "gar_last_error", "gar_aggregate_bcast", "gar_combine_bcast",
+           "gar_num_selected", "gar_check_args", "gar_status_string", "gar_last_error", "gar_aggregate_bcast", "gar_combine_bcast",
            "gar_aggregate_mcast", "gar_combine_mcast", "gar_trimmed_membership", "gar_aggregate_sgd",
            "gar_combine_sgd", "gar_nonfinite_rows", "sanitize", "aggregate_sanitized", "TooManyNonFinite"]

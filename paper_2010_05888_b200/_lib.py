@@ -48,6 +48,7 @@ def _load():
         "gar_last_error": ([], ctypes.c_char_p),
         "gar_workspace_bytes": ([I, I, I, I64], SZ),
         "gar_num_selected": ([I, I, I, I], I),
+        "gar_check_args": ([I, I, I, I], I),
         "gar_aggregate": ([I, PP, I, I, I64, P, P], I),
         "gar_aggregate_ex": ([I, PP, I, I, I, I64, P, P, P, SZ, P], I),
         "gar_select": ([I, PP, I, I, I, I64, P, IP, P, SZ, P], I),
@@ -232,6 +233,11 @@ def gar_last_error() -> str:
 
 def gar_workspace_bytes(rule, n: int, f: int, d: int) -> int:
     return int(lib.gar_workspace_bytes(rule_id(rule), n, f, d))
+
+
+def gar_check_args(rule, n: int, f: int, m: int = 0) -> int:
+    """The C library's argument status for (rule, n, f, m) (0 = GAR_OK)."""
+    return int(lib.gar_check_args(rule_id(rule), n, f, m))
 
 
 def gar_num_selected(rule, n: int, f: int, m: int = 0) -> int:

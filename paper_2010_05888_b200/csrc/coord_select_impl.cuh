@@ -357,6 +357,10 @@ __global__ void __launch_bounds__(32 * (W + kProducers), 1) coord_select_kernel(
       }
       store_result(p.out, p.extra, start + c, res, pv);
     }
+    // generic-proxy writes into the ring (the ragged-tail fill, Bulyan's sorted
+    // column park) must be ordered before the producer's next async-proxy
+    // (bulk copy) overwrite of this stage: PTX memory model, ADVICE r1
+    if (MODE == kModeBulyan || (c >= bulk_cnt && c < cnt)) fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
     if (++stage == stages) { stage = 0; phase ^= 1; }

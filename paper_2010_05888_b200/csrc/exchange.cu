@@ -49,12 +49,13 @@ __device__ __forceinline__ uint64_t global_ns() {
 // Block 0 publishes this rank's slot writes (they completed with the previous
 // kernel) to every rank's flag[rank]; every block then waits until all
 // `world` local flags reach `epoch` and sums the slots in rank order.  A wait
-// longer than ~10 s (a rank that never arrives) gives up and yields NaN
-// instead of hanging the GPU.
+// longer than ~10 s (a rank that never arrives) traps: the kernel fails, the
+// stream (and context) carry a sticky launch error that the next libgar /
+// CUDA call returns (GAR_ERR_CUDA), instead of hanging the GPU or handing a
+// plausible-looking selection to the caller.
 __global__ void __launch_bounds__(256) gram_gather_kernel(PeerFlags flags, int world, int rank, uint32_t epoch,
                                                           const double* __restrict__ local_slots, int nn,
                                                           double* __restrict__ G) {
-  __shared__ int ok;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     __threadfence_system();
     for (int r = 0; r < world; ++r) st_release_sys(flags.p[r] + rank, epoch);
@@ -62,25 +63,19 @@ __global__ void __launch_bounds__(256) gram_gather_kernel(PeerFlags flags, int w
   if (threadIdx.x == 0) {
     const uint32_t* mine = flags.p[rank];
     const uint64_t t0 = global_ns();
-    int good = 1;
     for (int r = 0; r < world; ++r) {
       while (static_cast<int32_t>(ld_acquire_sys(mine + r) - epoch) < 0) {
-        if (global_ns() - t0 > 10000000000ull) {
-          good = 0;
-          break;
-        }
+        if (global_ns() - t0 > 10000000000ull) __trap();
         __nanosleep(100);
       }
-      if (!good) break;
     }
-    ok = good;
   }
   __syncthreads();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nn) return;
   double s = 0.0;
   for (int r = 0; r < world; ++r) s += local_slots[static_cast<size_t>(r) * nn + e];
-  G[e] = ok ? s : __longlong_as_double(0x7ff8000000000000ll);
+  G[e] = s;
 }
 
 }  // namespace

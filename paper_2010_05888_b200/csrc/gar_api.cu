@@ -337,6 +337,8 @@ size_t gar_workspace_bytes(gar_rule rule, int n, int f, int64_t d) {
   return ws_bytes_for(n);
 }
 
+gar_status gar_check_args(gar_rule rule, int n, int f, int m) { return check_rule_args(rule, n, f, m); }
+
 int gar_num_selected(gar_rule rule, int n, int f, int m) {
   if (check_rule_args(rule, n, f, m) != GAR_OK) return 0;
   if (rule == GAR_BULYAN) return n - 2 * f;

@@ -9,9 +9,12 @@ namespace gar {
 // Upper bound on the number of per-CTA partial Gram matrices (>= SM count).
 constexpr int kGramMaxParts = 160;
 
-// Per-coordinate centring reference c_k (DESIGN.md §4 "Gram"): the median of
-// fin(x_0k), fin(x_1k), fin(x_2k) (fin(v) = v if finite else 0), or fin(x_0k)
-// when n < 3.  A per-coordinate translation: D_ij is unchanged mathematically.
+// Per-coordinate centring reference c_k (DESIGN.md §4 "Gram"): c_k =
+// fin(x_{r*,k}) (fin(v) = v if finite else 0), where r* is the most central
+// row of a 128-coordinate sample of the CTA's slice (gram_tc.cu center_pick:
+// smallest sum of the floor((n-1)/2) smallest sample distances).  Each CTA
+// picks its own r*; a per-coordinate translation leaves D_ij unchanged
+// mathematically.
 
 // Partial Gram matrices of the centred rows, one fp64 [n x n] per CTA,
 // written to partials[p*n*n ...].  *n_parts receives the number written.

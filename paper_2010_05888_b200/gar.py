@@ -18,21 +18,12 @@ class Aggregator:
         self.rid = _lib.rule_id(rule)
         self.n, self.f = int(n), int(f)
         self.m = 0 if m is None else int(m)
-        # argument check (quorum, m) without touching the GPU
-        if rule in ("krum", "multi_krum", "bulyan", "mda"):
-            if _lib.gar_num_selected(rule, self.n, self.f, self.m) == 0:
-                raise _lib.GarError(2 if self.m == 0 else 3, f"init({rule!r}, n={n}, f={f}, m={m})")
-        elif _lib.gar_workspace_bytes(rule, self.n, self.f, 0) == 0 and not self._coord_ok():
-            raise _lib.GarError(2, f"init({rule!r}, n={n}, f={f})")
+        # the library's own argument check (quorum, m, MDA budget) without touching the GPU
+        code = _lib.gar_check_args(rule, self.n, self.f, self.m)
+        if code != 0:
+            raise _lib.GarError(code, f"init({rule!r}, n={n}, f={f}, m={m})")
         self._ws = {}
         self._idx = {}
-
-    def _coord_ok(self):
-        if self.n < 1 or self.n > _lib.MAX_N or self.f < 0:
-            return False
-        if self.rule in ("median", "trimmed_mean", "mean_around_median"):
-            return self.n >= 2 * self.f + 1
-        return True
 
     @property
     def num_selected(self) -> int:

@@ -105,6 +105,34 @@ def test_select_rejects_coordinatewise_rules(gl):
     assert code == 5
 
 
+@pytest.mark.parametrize("rule,n,f,m,code", [
+    ("average", 7, 0, 0, 0), ("average", 7, 3, 0, 0), ("average", 7, 9, 0, 0),     # R15: Average ignores f
+    ("average", 7, -1, 0, 1), ("median", 7, 3, 0, 0), ("median", 7, 4, 0, 2),
+    ("multi_krum", 9, 2, 6, 3), ("multi_krum", 9, 2, 5, 0), ("bulyan", 11, 2, 0, 0), ("bulyan", 10, 2, 0, 2),
+    ("mda", 64, 20, 0, 5), ("mda", 9, 3, 0, 0), ("mda", 9, 5, 0, 2), ("median", 65, 0, 0, 1),
+])
+def test_check_args(gl, rule, n, f, m, code):
+    """gar_check_args: the status every entry point's host-side check returns
+    (MDA beyond its C(n, f) budget is GAR_ERR_UNSUPPORTED, not a quorum error)."""
+    assert gl.gar_check_args(rule, n, f, m) == code
+
+
+def test_average_accepts_any_f(gl):
+    """Reading R15: Average, the non-robust control, ignores f
+    (SPEC S:34 asks f = 0); the argument checks pass for any f >= 0."""
+    for f in (0, 1, 7, 40):
+        assert _call_ex(gl, "average", 31, f, 0, 100) in (1, 7)      # past the checks: device-pointer / CUDA stage
+    from paper_2010_05888_b200 import init
+    assert init("average", 31, 7).f == 7
+
+
+def test_mda_budget_reports_unsupported():
+    from paper_2010_05888_b200 import init, GarError
+    with pytest.raises(GarError) as e:
+        init("mda", 64, 20)
+    assert e.value.code == 5
+
+
 def test_python_binding_validates_before_gpu():
     import torch
     from paper_2010_05888_b200 import init, GarError

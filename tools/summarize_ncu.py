@@ -57,6 +57,7 @@ def main(rep, launches=None):
     hdr, units = rows[0], rows[1]
     out = []
     traffic = collections.defaultdict(list)
+    per_kernel = collections.defaultdict(list)
     print(f"## ncu --set full: `{os.path.basename(rep)}`\n")
     print("| kernel | " + " | ".join(KEYS.values()) + " | top stalls |")
     print("|---" * (len(KEYS) + 2) + "|")
@@ -83,8 +84,10 @@ def main(rep, launches=None):
         short = name.split("(")[0].replace("void ", "").replace("gar::", "").replace("<unnamed>::", "")
         print(f"| `{short}` | " + " | ".join(cells) + f" | {top} |")
         if "dram__bytes_read.sum" in d:
-            traffic[kclass(name)].append(to_bytes(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"])
-                                         + to_bytes(d["dram__bytes_write.sum"], u["dram__bytes_write.sum"]))
+            b = (to_bytes(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"])
+                 + to_bytes(d["dram__bytes_write.sum"], u["dram__bytes_write.sum"]))
+            traffic[kclass(name)].append(b)
+            per_kernel[short.split("<")[0]].append(b)
     summary = {k: int(sum(v) / len(v)) for k, v in traffic.items()}
     print("\nMean dram bytes (read + write) per launch, by kernel class: "
           + ", ".join(f"{k} {v / 1e9:.3f} GB" for k, v in summary.items()))
@@ -95,20 +98,24 @@ def main(rep, launches=None):
         h = lr[start]
         iname, ival, iunit = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
         per = collections.defaultdict(float)
+        cnt = collections.defaultdict(int)
         total = 0.0
         for r in lr[start + 1:]:
             if len(r) <= ival:
                 continue
-            c = kclass(r[iname])
-            if c == "other":
+            if kclass(r[iname]) == "other":
                 continue
+            nm = r[iname].split("(")[0].replace("void ", "").replace("gar::", "").replace("<unnamed>::", "")
             t = to_us(r[ival], r[iunit])
-            per[c] += t
+            per[nm] += t
+            cnt[nm] += 1
             total += t
-        print("| kernel class | total us (2 steps) | share |\n|---|---|---|")
+        print("| kernel | launches | total us | mean us per launch | share |\n|---|---|---|---|---|")
         for c, t in sorted(per.items(), key=lambda kv: -kv[1]):
-            print(f"| {c} | {t:.1f} | {t / total:.3f} |")
-    json.dump(summary, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
+            print(f"| `{c}` | {cnt[c]} | {t:.1f} | {t / cnt[c]:.1f} | {t / total:.3f} |")
+    json.dump({"per_class": summary, "per_kernel": {k: int(sum(v) / len(v)) for k, v in per_kernel.items()},
+               "source": os.path.basename(rep)},
+              open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
