@@ -16,7 +16,12 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int N, bool ATMEM, bool I8 = false>
+// kind::f16: D f32 (c_format 1), A/B fp16 (format 0), K-major
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+template <int N, bool ATMEM, bool I8 = false, bool F16 = false>
 __global__ void bench(int iters, long long* out) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ uint32_t slot;
@@ -39,7 +44,7 @@ __global__ void bench(int iters, long long* out) {
   const uint32_t tb = slot;
   if (threadIdx.x == 0) {
     const uint32_t a0 = smem_u32(base), b0 = smem_u32(base + 64 * 1024);
-    constexpr uint32_t id = I8 ? idesc_i8(128, N) : idesc_tf32(128, N);
+    constexpr uint32_t id = I8 ? idesc_i8(128, N) : F16 ? idesc_f16(128, N) : idesc_tf32(128, N);
     uint32_t phase = 0;
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
@@ -50,6 +55,11 @@ __global__ void bench(int iters, long long* out) {
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
                        ::"r"(tb + 256), "r"(tb + 8 * (kk & 7)), "l"(bd), "r"(id), "r"(acc));
+        } else if (F16) {
+          const uint64_t ad = sw128_desc(a0 + (kk & 3) * 32 + (kk >> 2) * 16384);
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                       ::"r"(tb + 256), "l"(ad), "l"(bd), "r"(id), "r"(acc));
         } else if (I8) {
           const uint64_t ad = sw128_desc(a0 + (kk & 3) * 32 + (kk >> 2) * 16384);
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -75,20 +85,21 @@ __global__ void bench(int iters, long long* out) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(512));
 }
 
-template <int N, bool AT, bool I8 = false>
+template <int N, bool AT, bool I8 = false, bool F16 = false>
 void run() {
   long long* d; cudaMalloc(&d, 148 * 8);
   const int smem = 100 * 1024;
-  cudaFuncSetAttribute(bench<N, AT, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(bench<N, AT, I8, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
-  bench<N, AT, I8><<<148, 128, smem>>>(iters, d);
-  bench<N, AT, I8><<<148, 128, smem>>>(iters, d);
+  bench<N, AT, I8, F16><<<148, 128, smem>>>(iters, d);
+  bench<N, AT, I8, F16><<<148, 128, smem>>>(iters, d);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double cyc = (double)h[0] / (iters * 16);
-  double macs = 128.0 * N * (I8 ? 32 : 8);
-  printf("%s M=128 N=%3d K=%d A from %s: %6.1f cycles/MMA, %6.0f MAC/clk/SM (%s)\n", I8 ? "i8  " : "tf32", N,
-         I8 ? 32 : 8, AT ? "TMEM" : "smem", cyc, macs / cyc, cudaGetErrorString(e));
+  const int K = I8 ? 32 : F16 ? 16 : 8;
+  double macs = 128.0 * N * K;
+  printf("%s M=128 N=%3d K=%d A from %s: %6.1f cycles/MMA, %6.0f MAC/clk/SM (%s)\n",
+         I8 ? "i8  " : F16 ? "f16 " : "tf32", N, K, AT ? "TMEM" : "smem", cyc, macs / cyc, cudaGetErrorString(e));
   cudaFree(d);
 }
 
@@ -96,5 +107,7 @@ int main() {
   run<64, false>(); run<128, false>(); run<256, false>();
   run<64, true>(); run<128, true>(); run<256, true>();
   run<64, false, true>(); run<96, false, true>(); run<128, false, true>(); run<256, false, true>();
+  run<64, false, false, true>(); run<128, false, false, true>(); run<192, false, false, true>();
+  run<256, false, false, true>();
   return 0;
 }
