@@ -11,7 +11,7 @@ configs[2] (ResNet-50-sized gradients, n=31, f=7, d=25,557,032: the config the
 north_star targets and scales to 8 GPUs); inputs (3.17 GB) exceed the 126 MB
 L2, so no flush is needed between steps.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--dtype bf16]
     torchrun --nproc-per-node N bench.py --gpus N ...   (d-sharded, NCCL)
 """
 from __future__ import annotations
@@ -45,6 +45,10 @@ def parse():
     ap.add_argument("--workload", default="C3", help="C1..C4 or sweep:<n>")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"],
+                    help="element type of the gradients (bf16: SURVEY §8f-4, widened exactly, DESIGN.md R16)")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the bf16 variant measured after the fp32 line's timed region (N=1)")
     ap.add_argument("--output", default="fused",
                     choices=["replicated", "replicated-async", "sharded", "fused", "fused-mc"],
                     help="N>1: all-gather the aggregate to every rank with NCCL (north_star), write it into every "
@@ -68,15 +72,16 @@ def peaks():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def rule_bytes(rule, n, f, d):
-    """Algorithmic HBM bytes of one aggregation."""
+def rule_bytes(rule, n, f, d, es=4):
+    """Algorithmic HBM bytes of one aggregation: input rows of
+    es bytes per coordinate read, the fp32 output written."""
     if rule in ("average", "median", "trimmed_mean"):
-        return 4 * d * (n + 1)
+        return es * d * n + 4 * d
     if rule == "krum":
-        return 4 * d * (n + 2)
+        return es * d * (n + 1) + 4 * d
     if rule == "multi_krum":
-        return 4 * d * (n + (n - f - 2) + 1)
-    return 4 * d * (n + (n - 2 * f) + 1)
+        return es * d * (n + (n - f - 2)) + 4 * d
+    return es * d * (n + (n - 2 * f)) + 4 * d
 
 
 class Clocks:
@@ -171,6 +176,12 @@ def run_ours(args):
     lo, hi = synth.shard_bounds(d, rank, world) if world > 1 else (0, d)
     dl = hi - lo
     X = synth.make_gradients(n, f, dl, seed=synth.BASE_SEED + 2 + 1000 * rank, device=dev)
+    bf16 = args.dtype == "bf16"
+    if bf16:
+        X = synth.to_bf16(X)
+        if world > 1 and args.output not in ("replicated", "sharded"):
+            args.output = "replicated"          # fused outputs take fp32 rows (dist._LibgarBackend)
+    es = X.element_size()
     torch.cuda.synchronize()
 
     from paper_2010_05888_b200.dist import ShardedAggregator, shard_len
@@ -182,20 +193,19 @@ def run_ours(args):
     # kernel class of the stage ending at each mark (DESIGN.md §8 roofline bookkeeping)
     CLASS = {"gram": "gram", "exchange": "exchange", "select": "select", "combine": "coord_select",
              "coord": "coord_select", "gather": "gather"}
-    segs = []          # (kernel class, rule, start event, end event)
 
     def ev():
         e = torch.cuda.Event(enable_timing=True)
         e.record(stream)
         return e
 
-    def step(record):
+    def step(Xin, segs):
         # fused output: one cross-GPU barrier per step (the last rule's), which
         # makes all six replicated outputs readable (dist.ShardedAggregator.sync)
         for r in RULES:
             last_rule = r == RULES[-1]
-            if not record:
-                aggs[r].aggregate(X, out_local=outs[r], out_full=full[r], barrier=last_rule)
+            if segs is None:
+                aggs[r].aggregate(Xin, out_local=outs[r], out_full=full[r], barrier=last_rule)
                 continue
             last = [ev()]
 
@@ -203,31 +213,39 @@ def run_ours(args):
                 e = ev()
                 segs.append((label, r, last[0], e))
                 last[0] = e
-            aggs[r].aggregate(X, out_local=outs[r], out_full=full[r], mark=mark, barrier=last_rule)
+            aggs[r].aggregate(Xin, out_local=outs[r], out_full=full[r], mark=mark, barrier=last_rule)
         for r in RULES:              # output="replicated-async": the step ends when every gather has
             aggs[r].wait()           # landed (they overlap the following rules' kernels)
 
-    for _ in range(args.warmup):
-        step(False)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    with Clocks(local) as clk:
+    def measure(Xin, steps, warmup, clocks=True):
+        """(ms over `steps` steps, segments, clock summary), max over ranks."""
+        segs = []
+        for _ in range(warmup):
+            step(Xin, None)
         torch.cuda.synchronize()
-        t0 = ev()
-        for _ in range(args.steps):
-            step(True)
-        t1 = ev()
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = t0.elapsed_time(t1)
-    # per-segment device times
-    cls_ms, rule_ms = {}, {r: 0.0 for r in RULES}
-    for lab, r, a, b in segs:
-        t = a.elapsed_time(b)
-        cls_ms[CLASS[lab]] = cls_ms.get(CLASS[lab], 0.0) + t
-        rule_ms[r] += t
+        if world > 1:
+            dist.barrier()
+        with Clocks(local) as clk:
+            torch.cuda.synchronize()
+            t0 = ev()
+            for _ in range(steps):
+                step(Xin, segs)
+            t1 = ev()
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return t0.elapsed_time(t1), segs, clk.summary()
+
+    def rule_times(segs):
+        cls_ms, rule_ms = {}, {r: 0.0 for r in RULES}
+        for lab, r, a, b in segs:
+            t = a.elapsed_time(b)
+            cls_ms[CLASS[lab]] = cls_ms.get(CLASS[lab], 0.0) + t
+            rule_ms[r] += t
+        return cls_ms, rule_ms
+
+    ms, segs, clocks = measure(X, args.steps, args.warmup)
+    cls_ms, rule_ms = rule_times(segs)
     if world > 1:
         t = torch.tensor([ms] + [rule_ms[r] for r in RULES], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -240,7 +258,7 @@ def run_ours(args):
     # double-buffered, so step k+1's H2D overlaps step k's aggregation and D2H.
     e2e = None
     if args.e2e_steps > 0:
-        host_x = torch.empty(X.shape, dtype=torch.float32, pin_memory=True)
+        host_x = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
         host_x.copy_(X)
         host_out = [{r: torch.empty(dl, dtype=torch.float32, pin_memory=True) for r in RULES} for _ in range(2)]
         xbuf = [X, torch.empty_like(X)]
@@ -301,94 +319,122 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t[0])
         del xbuf[1], fbuf[1]
-        e2e = {"value": round(len(RULES) * n * d * 4 / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
-               "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": int(X.numel() * 4 * world),
+        e2e = {"value": round(len(RULES) * n * d * es / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": int(X.numel() * es * world),
                "d2h_bytes_per_step": int(len(RULES) * dl * 4 * world),
-               "path": ("paper_2010_05888_b200.init(rule, n, f).aggregate(X) per rule (one gar_aggregate_ex C call "
-                        "each)" if world == 1 else
+               "path": ("paper_2010_05888_b200.init(rule, n, f).aggregate(X) per rule (one "
+                        + ("gar_aggregate_dt" if bf16 else "gar_aggregate_ex") + " C call each)" if world == 1 else
                         "dist.ShardedAggregator.aggregate per rule (gar_gram_exchange / gar_select_from_gram / "
                         "gar_combine_bcast for the Krum family, gar_aggregate_bcast otherwise)")
                        + "; inputs H2D from pinned host and six results D2H every step, on copy streams, "
                          "double-buffered so step k+1's H2D overlaps step k's aggregation"}
 
+    # ---- the bf16 variant of the same workload, after the
+    # timed region of the line: same bits rounded to bf16, same step
+    variant = None
+    if world == 1 and not bf16 and not args.no_variants:
+        X16 = synth.to_bf16(X)
+        ms16, segs16, clk16 = measure(X16, args.steps, max(args.warmup, 3))
+        del X16
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     peak, peak_src = peaks()
-    ms_step = ms / args.steps
-    grad_bytes = len(RULES) * n * d * 4
-    value = grad_bytes / (ms_step * 1e-3) / 1e9
-    # ---- per-kernel roofline: every timed segment is one
-    # libgar kernel launch, except "gram", which is the Gram kernel plus the
-    # deterministic n x n partial reduction (~1 % of it; counted against the
-    # Gram, so its fraction is conservative).  Algorithmic bytes per launch on
-    # this rank's slice: rows read + output written.
     m_mk, theta = n - f - 2, n - 2 * f
     np_ = 8 if n <= 8 else 16 if n <= 16 else 32 if n <= 32 else 64
-    kern = {}
 
-    def add(name, t_ms, nbytes):
-        k = kern.setdefault(name, {"ms_per_step": 0.0, "launches_per_step": 0, "bytes": 0})
-        k["ms_per_step"] += t_ms / args.steps
-        k["launches_per_step"] += 1
-        k["bytes"] += nbytes
-    seg_name = {"combine": {"krum": ("copy_row_kernel", 4 * dl * 2),
-                            "multi_krum": ("coord_select_kernel<average of m selected rows>", 4 * dl * (m_mk + 1)),
-                            "bulyan": ("coord_select_kernel<bulyan coordinate phase>", 4 * dl * (theta + 1))}}
-    for lab, r, a, b in segs:
-        t = a.elapsed_time(b)
-        if lab == "gram":
-            add(f"gram_tc_kernel<{np_}>", t, 4 * n * dl)
-        elif lab == "select":
-            add("select_kernel", t, 0)
-        elif lab == "combine":
-            add(*((seg_name["combine"][r][0], t, seg_name["combine"][r][1])))
-        elif lab == "coord":
-            add(f"coord_select_kernel<{r}>", t, 4 * dl * (n + 1))
-    reps = args.steps   # every segment was recorded once per rule per step
-    kernels = {}
-    for name, k in kern.items():
-        per_launch_ms = k["ms_per_step"] * reps / k["launches_per_step"]     # average launch duration
-        per_launch_bytes = k["bytes"] / k["launches_per_step"]
-        ach = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 and per_launch_bytes else 0.0
-        kernels[name] = {"ms_per_step": round(k["ms_per_step"], 4),
-                         "launches_per_step": k["launches_per_step"] // reps,
-                         "ms_per_launch": round(per_launch_ms, 4),
-                         "algorithmic_bytes_per_launch": int(per_launch_bytes),
-                         "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 4) if ach else None,
-                         "share_of_step": round(k["ms_per_step"] / ms_step, 4)}
+    def kernel_table(segs, ms_step, esz):
+        """Per-kernel roofline: every timed segment is one
+        libgar kernel launch, except "gram", which is the Gram kernel plus the
+        deterministic n x n partial reduction (~1 % of it; counted against the
+        Gram, so its fraction is conservative).  Algorithmic bytes per launch on
+        this rank's slice: rows read (esz bytes per coordinate) + fp32 output."""
+        kern = {}
+
+        def add(name, t_ms, nbytes):
+            k = kern.setdefault(name, {"ms_per_step": 0.0, "launches_per_step": 0, "bytes": 0})
+            k["ms_per_step"] += t_ms / args.steps
+            k["launches_per_step"] += 1
+            k["bytes"] += nbytes
+        seg_name = {"krum": ("copy_row_kernel", (esz + 4) * dl),
+                    "multi_krum": ("coord_select_kernel<average of m selected rows>", (esz * m_mk + 4) * dl),
+                    "bulyan": ("coord_select_kernel<bulyan coordinate phase>", (esz * theta + 4) * dl)}
+        for lab, r, a, b in segs:
+            t = a.elapsed_time(b)
+            if lab == "gram":
+                add(f"gram_tc_kernel<{np_}>", t, esz * n * dl)
+            elif lab == "select":
+                add("select_kernel", t, 0)
+            elif lab == "combine":
+                add(seg_name[r][0], t, seg_name[r][1])
+            elif lab == "coord":
+                add(f"coord_select_kernel<{r}>", t, (esz * n + 4) * dl)
+        reps = args.steps   # every segment was recorded once per rule per step
+        kernels = {}
+        for name, k in kern.items():
+            per_launch_ms = k["ms_per_step"] * reps / k["launches_per_step"]     # average launch duration
+            per_launch_bytes = k["bytes"] / k["launches_per_step"]
+            ach = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 and per_launch_bytes else 0.0
+            kernels[name] = {"ms_per_step": round(k["ms_per_step"], 4),
+                             "launches_per_step": k["launches_per_step"] // reps,
+                             "ms_per_launch": round(per_launch_ms, 4),
+                             "algorithmic_bytes_per_launch": int(per_launch_bytes),
+                             "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 4) if ach else None,
+                             "share_of_step": round(k["ms_per_step"] / ms_step, 4)}
+        return kernels
+
+    def per_rule_table(rms, esz):
+        out = {}
+        for r in RULES:
+            t = rms[r] / args.steps
+            out[r] = {"ms": round(t, 4), "grad_gbs": round(n * d * esz / (t * 1e-3) / 1e9, 1),
+                      "roofline_frac": round(rule_bytes(r, n, f, d, esz) / world / (t * 1e-3) / 1e9 / peak, 4)}
+        return out
+
+    ms_step = ms / args.steps
+    grad_bytes = len(RULES) * n * d * es
+    value = grad_bytes / (ms_step * 1e-3) / 1e9
+    kernels = kernel_table(segs, ms_step, es)
     dom = max((k for k in kernels if kernels[k]["algorithmic_bytes_per_launch"]),
               key=lambda k: kernels[k]["ms_per_step"])
     # libgar kernels per step: 1 per coordinate-wise rule; per Krum-family rule
     # Gram partials + reduction + selection + combine, and with the peer-memory
     # exchange (N > 1) the reduction is a reduce-and-store plus a gather kernel
-    peer = world > 1 and aggs["krum"]._use_peer_exchange(dev)
+    peer = world > 1 and aggs["krum"]._use_peer_exchange(dev, X)
     launches_per_step = 3 + 3 * (5 if peer else 4)
     stages = {c: round(t / args.steps, 4) for c, t in sorted(cls_ms.items())}
-    per_rule = {}
-    for r in RULES:
-        t = rule_ms[r] / args.steps
-        per_rule[r] = {"ms": round(t, 4), "grad_gbs": round(n * d * 4 / (t * 1e-3) / 1e9, 1),
-                       "roofline_frac": round(rule_bytes(r, n, f, d) / world / (t * 1e-3) / 1e9 / peak, 4)}
+    per_rule = per_rule_table(rule_ms, es)
+    if world == 1 and not bf16 and not args.no_variants:
+        ms16_step = ms16 / args.steps
+        k16 = kernel_table(segs16, ms16_step, 2)
+        variant = {"bf16": {
+            "what": "the same step on the same gradients rounded to bf16 (gar_*_dt, exact widening, DESIGN.md R16), "
+                    "measured after this line's timed region; gradient bytes n*d*2",
+            "value": round(len(RULES) * n * d * 2 / (ms16_step * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "ms_per_step": round(ms16_step, 4), "speedup_vs_f32": round(ms_step / ms16_step, 3),
+            "per_rule": per_rule_table(rule_times(segs16)[1], 2), "kernels": k16, "clocks": clk16}}
+    metric = METRIC if not bf16 else METRIC.replace("n*d*4B", "n*d*2B bf16")
     line = {
-        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "metric": metric, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16" if bf16 else "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: n={n} f={f} d={d}, GARs {'/'.join(RULES)}",
                    "n": n, "f": f, "d": d, "parallelism": f"d-sharded x{world}" if world > 1 else "single GPU",
                    "output": (args.output + (f" ({aggs[RULES[0]].fused_path})" if aggs[RULES[0]].fused_path else ""))
                    if world > 1 else "local",
-                   "l2": f"inputs {n * d * 4 / 1e9:.2f} GB > 126 MB L2 (no flush needed)"},
+                   "l2": f"inputs {n * d * es / 1e9:.2f} GB > 126 MB L2 (no flush needed)"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": kernels[dom]["frac"],
                      "algorithmic_bytes_per_launch": kernels[dom]["algorithmic_bytes_per_launch"],
                      "launches_per_step": kernels[dom]["launches_per_step"],
                      "share_of_step": kernels[dom]["share_of_step"],
-                     "traffic": traffic_from_profiles(dom, args.workload, world)},
-        "kernels": kernels, "per_rule": per_rule, "clocks": clk.summary(),
+                     "traffic": traffic_from_profiles(dom, args.workload, world) if not bf16 else None},
+        "kernels": kernels, "per_rule": per_rule, "clocks": clocks,
         "stages_ms": stages, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
     }
+    if variant:
+        line["variants"] = variant
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, X, d)
     print(json.dumps(line), flush=True)
@@ -405,10 +451,14 @@ def oracle_step(x, f):
 
 def cpu_baseline(cfg, X, d, reps=3):
     """The oracle, as it stands, on the box's host cores over the SAME resident
-    workload (copied to host): all six GARs once per repetition, median of
-    `reps` (about 10-30 s of CPU work at C3)."""
+    workload (copied to host; bf16 rows widened exactly first, R16): all six
+    GARs once per repetition, median of `reps` (about 10-30 s of CPU work at C3)."""
     import oracle
-    x = X[:, :d].cpu().numpy()
+    import torch
+    if X.dtype == torch.bfloat16:
+        x = oracle.widen_bf16(synth.bf16_bits(X[:, :d]))
+    else:
+        x = X[:, :d].cpu().numpy()
     x = x if x.flags["C_CONTIGUOUS"] else x.copy()
     times = []
     for _ in range(reps):

@@ -251,6 +251,42 @@ gar_status gar_nonfinite_rows(const float* const* grads, int n, int64_t d, uint6
 gar_status gar_trimmed_membership(const float* const* grads, int n, int f, int64_t d,
                                   uint64_t* mask_dev, gar_stream_t stream);
 
+/* ---- bf16 gradient rows (R16) ---------------------
+ * Not in the paper: its gradients are fp32 tensors.
+ * Reading R16: a bf16 input is widened EXACTLY to fp32 and every rule is the
+ * fp32 definition applied to the widened values (same canonical order,
+ * fp64 averages rounded once to fp32, squared distances, ties to the lower
+ * index); outputs stay fp32.  The _dt entry points are the fp32 calls of the
+ * same name with a dtype argument and untyped row pointers:
+ *   dtype  GAR_F32 (rows are fp32[d]) or GAR_BF16 (rows are bf16[d], the
+ *          upper 16 bits of an IEEE fp32, e.g. torch.bfloat16);
+ *          anything else -> GAR_ERR_INVALID_ARGUMENT;
+ *   grads  host array of n DEVICE pointers, each 16-byte aligned (bf16 rows
+ *          are read with 16-byte bulk copies: 8 coordinates per granule);
+ *   out    DEVICE fp32[d], 16-byte aligned, not overlapping any row's
+ *          [0, d * elem_size) bytes.
+ * Argument checks, statuses, workspace sizes (gar_workspace_bytes) and the
+ * execution model are those of the fp32 calls. */
+typedef enum { GAR_F32 = 0, GAR_BF16 = 1 } gar_dtype;
+
+gar_status gar_aggregate_dt(gar_rule rule, gar_dtype dtype, const void* const* grads, int n, int f, int m,
+                            int64_t d, float* out, int32_t* indices_dev, void* workspace,
+                            size_t workspace_bytes, gar_stream_t stream);
+
+gar_status gar_select_dt(gar_rule rule, gar_dtype dtype, const void* const* grads, int n, int f, int m,
+                         int64_t d, int32_t* indices_dev, int* n_selected_host, void* workspace,
+                         size_t workspace_bytes, gar_stream_t stream);
+
+gar_status gar_distances_dt(gar_dtype dtype, const void* const* grads, int n, int64_t d, double* D_dev,
+                            void* workspace, size_t workspace_bytes, gar_stream_t stream);
+
+gar_status gar_gram_partial_dt(gar_dtype dtype, const void* const* grads, int n, int64_t d_local,
+                               double* gram_dev, void* workspace, size_t workspace_bytes,
+                               gar_stream_t stream);
+
+gar_status gar_combine_dt(gar_rule rule, gar_dtype dtype, const void* const* grads, int n, int f, int m,
+                          int64_t d_local, const int32_t* indices_dev, float* out, gar_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -303,6 +303,27 @@ def median3_reorder(v):
     return w
 
 
+def widen_bf16(bits):
+    """bf16 -> fp32, exactly (R16; SURVEY §8f-4 "bf16 gradient inputs").
+
+    A bf16 value is, by definition, the upper 16 bits of an IEEE-754 binary32
+    (same sign bit, same 8-bit exponent, the 7 leading fraction bits), so its
+    fp32 value is the 32-bit word ``bits << 16``.  Every bf16 value (NaN, +-inf,
+    +-0 and subnormals included) is representable in fp32; the widening rounds
+    nothing.  Reading R16: a rule over bf16 inputs is the fp32 rule over the
+    widened values, so the oracle of a bf16 call is this widening followed by
+    the fp32 oracle below -- no other arithmetic changes."""
+    b = np.ascontiguousarray(bits)
+    if b.dtype != np.uint16:
+        raise TypeError("bf16 inputs are given as their uint16 bit patterns")
+    return (b.astype(np.uint32) << np.uint32(16)).view(np.float32)
+
+
+def aggregate_bf16(rule, bits, f, m=None, threads=None):
+    """aggregate() of bf16 inputs (uint16 bit patterns [n, d]): R16."""
+    return aggregate(rule, widen_bf16(bits), f, m, threads)
+
+
 def aggregate(rule, x, f, m=None, threads=None):
     """Dispatch by rule name (test convenience). Returns (out, selected or None)."""
     if rule == "average":

@@ -26,6 +26,8 @@ RULES = {"average": 0, "median": 1, "trimmed_mean": 2, "krum": 3, "multi_krum": 
 STATUS = {0: "GAR_OK", 1: "GAR_ERR_INVALID_ARGUMENT", 2: "GAR_ERR_QUORUM", 3: "GAR_ERR_INVALID_M",
           4: "GAR_ERR_ALIGNMENT", 5: "GAR_ERR_UNSUPPORTED", 6: "GAR_ERR_WORKSPACE", 7: "GAR_ERR_CUDA"}
 MAX_N = 64
+# gar_dtype (include/gar.h): element type of the gradient rows
+DTYPES = {torch.float32: 0, torch.bfloat16: 1}
 
 
 class GarError(RuntimeError):
@@ -65,6 +67,11 @@ def _load():
         "gar_gram_exchange": ([PP, I, I64, PP, PP, I, I, ctypes.c_uint32, P, PP, P, SZ, P], I),
         "gar_aggregate_sgd": ([I, PP, I, I, I, I64, P, ctypes.c_float, P, P, SZ, P], I),
         "gar_combine_sgd": ([I, PP, I, I, I, I64, P, P, ctypes.c_float, P], I),
+        "gar_aggregate_dt": ([I, I, PP, I, I, I, I64, P, P, P, SZ, P], I),
+        "gar_select_dt": ([I, I, PP, I, I, I, I64, P, IP, P, SZ, P], I),
+        "gar_distances_dt": ([I, PP, I, I64, P, P, SZ, P], I),
+        "gar_gram_partial_dt": ([I, PP, I, I64, P, P, SZ, P], I),
+        "gar_combine_dt": ([I, I, PP, I, I, I, I64, P, P, P], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -125,22 +132,28 @@ class DevicePtrRows:
 
 
 def row_pointers(grads, d: int | None = None):
-    """(ctypes void* array, n, d) from a list of 1-D fp32 CUDA tensors or a
-    2-D [n, ld] fp32 CUDA tensor with unit column stride.  For a matrix the
-    row pointers are base + i * row_stride (no per-row tensor views), and the
-    ctypes array is cached per (base, n, stride)."""
+    """(ctypes void* array, n, d, device) from a list of 1-D fp32 CUDA tensors
+    or a 2-D [n, ld] fp32 CUDA tensor with unit column stride.  For a matrix
+    the row pointers are base + i * row_stride (no per-row tensor views), and
+    the ctypes array is cached per (base, n, stride)."""
+    return row_pointers_dt(grads, d, (torch.float32,))[:4]
+
+
+def row_pointers_dt(grads, d: int | None = None, dtypes=(torch.float32, torch.bfloat16)):
+    """row_pointers for rows of any dtype in `dtypes`; returns (array, n, d,
+    device, gar_dtype code).  Raw DevicePtrRows are fp32 (code 0)."""
     if isinstance(grads, DevicePtrRows):
         n = len(grads)
         if not 1 <= n <= MAX_N:
             raise ValueError(f"n = {n} outside [1, {MAX_N}]")
         if d is None:
             raise ValueError("d is required with raw row addresses")
-        return grads._arr, n, d, grads.device
+        return grads._arr, n, d, grads.device, 0
     if isinstance(grads, torch.Tensor):
         if grads.dim() != 2:
             raise ValueError("a gradient matrix must be 2-D [n, ld]")
-        if grads.dtype != torch.float32:
-            raise TypeError("gradients must be float32")
+        if grads.dtype not in dtypes:
+            raise TypeError(f"gradients must be {' or '.join(str(t) for t in dtypes)}, not {grads.dtype}")
         if grads.device.type != "cuda":
             raise ValueError("gradients must live on a CUDA device (no CPU fallback)")
         n, ld = grads.shape
@@ -152,7 +165,7 @@ def row_pointers(grads, d: int | None = None):
             d = ld
         elif d > ld:
             raise ValueError("a gradient is shorter than d")
-        base, rs = grads.data_ptr(), grads.stride(0) * 4
+        base, rs = grads.data_ptr(), grads.stride(0) * grads.element_size()
         key = (base, n, rs)
         arr = _PTR_CACHE.get(key)
         if arr is None:
@@ -160,15 +173,17 @@ def row_pointers(grads, d: int | None = None):
                 _PTR_CACHE.clear()
             arr = (ctypes.c_void_p * n)(*[base + i * rs for i in range(n)])
             _PTR_CACHE[key] = arr
-        return arr, n, d, grads.device
+        return arr, n, d, grads.device, DTYPES[grads.dtype]
     rows = list(grads)
     n = len(rows)
     if not 1 <= n <= MAX_N:
         raise ValueError(f"n = {n} outside [1, {MAX_N}]")
     dev = rows[0].device
+    dt = rows[0].dtype
     for r in rows:
-        if r.dtype != torch.float32:
-            raise TypeError("gradients must be float32")
+        if r.dtype not in dtypes or r.dtype != dt:
+            raise TypeError(f"gradients must all be {' or '.join(str(t) for t in dtypes)} (one dtype), "
+                            f"not {r.dtype}")
         if r.device != dev or r.device.type != "cuda":
             raise ValueError("gradients must all live on the same CUDA device (no CPU fallback)")
         if r.dim() != 1 or (r.numel() > 1 and r.stride(0) != 1):
@@ -178,7 +193,7 @@ def row_pointers(grads, d: int | None = None):
     elif any(r.numel() < d for r in rows):
         raise ValueError("a gradient is shorter than d")
     arr = (ctypes.c_void_p * n)(*[r.data_ptr() for r in rows])
-    return arr, n, d, dev
+    return arr, n, d, dev, DTYPES[dt]
 
 
 def stream_handle(device, stream=None):
@@ -413,3 +428,49 @@ def gar_nonfinite_rows(grads, mask: torch.Tensor, d: int | None = None, stream=N
     mk = _buf(mask, (torch.int64, torch.uint64), 1, dev, "mask")
     check(lib.gar_nonfinite_rows(arr, n, d, mk, stream_handle(dev, stream)), "gar_nonfinite_rows")
     return mask
+
+
+# ------------------------------------------------------------------ bf16 rows (gar.h "_dt" entry points)
+def gar_aggregate_dt(rule, grads, f: int, m: int, out: torch.Tensor, indices=None, workspace=None,
+                     d: int | None = None, stream=None):
+    """gar_aggregate_ex for fp32 or bf16 rows (dtype from the tensors); out fp32."""
+    arr, n, d, dev, dt = row_pointers_dt(grads, d)
+    o, ix = _f32(out, d, dev), _idx(indices, rule, n, f, m, dev, True)
+    check(lib.gar_aggregate_dt(rule_id(rule), dt, arr, n, f, m, d, o, ix, _ptr(workspace), _wsb(workspace),
+                               stream_handle(dev, stream)), "gar_aggregate_dt")
+    return out
+
+
+def gar_select_dt(rule, grads, f: int, m: int, indices: torch.Tensor, workspace: torch.Tensor,
+                  d: int | None = None, stream=None) -> int:
+    arr, n, d, dev, dt = row_pointers_dt(grads, d)
+    nsel = ctypes.c_int(0)
+    ix = _idx(indices, rule, n, f, m, dev, False)
+    check(lib.gar_select_dt(rule_id(rule), dt, arr, n, f, m, d, ix, ctypes.byref(nsel), _ptr(workspace),
+                            _wsb(workspace), stream_handle(dev, stream)), "gar_select_dt")
+    return nsel.value
+
+
+def gar_distances_dt(grads, D: torch.Tensor, workspace: torch.Tensor, d: int | None = None, stream=None):
+    arr, n, d, dev, dt = row_pointers_dt(grads, d)
+    dp = _buf(D, torch.float64, n * n, dev, "D")
+    check(lib.gar_distances_dt(dt, arr, n, d, dp, _ptr(workspace), _wsb(workspace), stream_handle(dev, stream)),
+          "gar_distances_dt")
+    return D
+
+
+def gar_gram_partial_dt(grads, gram: torch.Tensor, workspace: torch.Tensor, d: int | None = None, stream=None):
+    arr, n, d, dev, dt = row_pointers_dt(grads, d)
+    g = _buf(gram, torch.float64, n * n, dev, "gram")
+    check(lib.gar_gram_partial_dt(dt, arr, n, d, g, _ptr(workspace), _wsb(workspace), stream_handle(dev, stream)),
+          "gar_gram_partial_dt")
+    return gram
+
+
+def gar_combine_dt(rule, grads, f: int, m: int, indices: torch.Tensor, out: torch.Tensor, d: int | None = None,
+                   stream=None):
+    arr, n, d, dev, dt = row_pointers_dt(grads, d)
+    ix, o = _idx(indices, rule, n, f, m, dev, False), _f32(out, d, dev)
+    check(lib.gar_combine_dt(rule_id(rule), dt, arr, n, f, m, d, ix, o, stream_handle(dev, stream)),
+          "gar_combine_dt")
+    return out

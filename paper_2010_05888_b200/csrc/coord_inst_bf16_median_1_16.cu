@@ -1,0 +1,7 @@
+// GENERATED instantiation unit (split for parallel compilation): bf16 rows.
+#include "coord_select_impl.cuh"
+namespace gar {
+cudaError_t launch_coord_median_1_16_bf16(const CoordLaunch& L, cudaStream_t stream) {
+  return dispatch_range<kModeMedian, 1, 16, bf2>(L, stream);
+}
+}  // namespace gar

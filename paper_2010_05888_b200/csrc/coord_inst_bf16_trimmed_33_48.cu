@@ -1,0 +1,7 @@
+// GENERATED instantiation unit (split for parallel compilation): bf16 rows.
+#include "coord_select_impl.cuh"
+namespace gar {
+cudaError_t launch_coord_trimmed_33_48_bf16(const CoordLaunch& L, cudaStream_t stream) {
+  return dispatch_range<kModeTrimmed, 33, 48, bf2>(L, stream);
+}
+}  // namespace gar

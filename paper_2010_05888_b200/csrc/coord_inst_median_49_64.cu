@@ -2,6 +2,6 @@
 #include "coord_select_impl.cuh"
 namespace gar {
 cudaError_t launch_coord_median_49_64(const CoordLaunch& L, cudaStream_t stream) {
-  return dispatch_range<kModeMedian, 49, 64>(L, stream);
+  return dispatch_range<kModeMedian, 49, 64, float>(L, stream);
 }
 }  // namespace gar

@@ -2,6 +2,6 @@
 #include "coord_select_impl.cuh"
 namespace gar {
 cudaError_t launch_coord_trimmed_1_16(const CoordLaunch& L, cudaStream_t stream) {
-  return dispatch_range<kModeTrimmed, 1, 16>(L, stream);
+  return dispatch_range<kModeTrimmed, 1, 16, float>(L, stream);
 }
 }  // namespace gar

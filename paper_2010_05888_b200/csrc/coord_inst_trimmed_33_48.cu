@@ -2,6 +2,6 @@
 #include "coord_select_impl.cuh"
 namespace gar {
 cudaError_t launch_coord_trimmed_33_48(const CoordLaunch& L, cudaStream_t stream) {
-  return dispatch_range<kModeTrimmed, 33, 48>(L, stream);
+  return dispatch_range<kModeTrimmed, 33, 48, float>(L, stream);
 }
 }  // namespace gar

@@ -10,7 +10,7 @@ namespace gar {
 enum CoordMode { kModeAverage = 0, kModeMedian = 1, kModeTrimmed = 2, kModeBulyan = 3 };
 
 struct CoordLaunch {
-  const float* const* rows;   // host array of n device row pointers
+  const float* const* rows;   // host array of n device row pointers (bf16 rows: type-punned)
   int n;                      // number of input rows
   const int32_t* idx;         // device: R selected indices (any order) or nullptr
   int R;                      // rows consumed per coordinate (n, m or theta)
@@ -19,6 +19,7 @@ struct CoordLaunch {
   float* out;                 // device fp32[d]
   OutPtrs extra;              // further destinations (n = 0: none)
   int num_sms;
+  int dtype;                  // ElemType (elem.cuh): kF32 or kBF16
 };
 
 cudaError_t launch_coord_select(int mode, const CoordLaunch& L, cudaStream_t stream);

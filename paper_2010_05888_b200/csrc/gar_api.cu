@@ -11,6 +11,7 @@
 #include "../../include/gar.h"
 #include "common.cuh"
 #include "coord_select.h"
+#include "elem.cuh"
 #include "gram.h"
 
 namespace {
@@ -78,12 +79,15 @@ gar_status check_rows(const float* const* grads, int n, int64_t d) {
   return GAR_OK;
 }
 
-gar_status check_out(const float* const* grads, int n, int64_t d, const float* out) {
+bool valid_dtype(int t) { return t == GAR_F32 || t == GAR_BF16; }
+uintptr_t elem_bytes(gar_dtype t) { return t == GAR_BF16 ? 2u : 4u; }
+
+gar_status check_out(const float* const* grads, int n, int64_t d, const float* out, gar_dtype dt = GAR_F32) {
   if (!out) return GAR_ERR_INVALID_ARGUMENT;
   if (reinterpret_cast<uintptr_t>(out) & 15u) return GAR_ERR_ALIGNMENT;
   const uintptr_t o0 = reinterpret_cast<uintptr_t>(out), o1 = o0 + uintptr_t(d) * 4u;
   for (int i = 0; i < n; ++i) {
-    const uintptr_t g0 = reinterpret_cast<uintptr_t>(grads[i]), g1 = g0 + uintptr_t(d) * 4u;
+    const uintptr_t g0 = reinterpret_cast<uintptr_t>(grads[i]), g1 = g0 + uintptr_t(d) * elem_bytes(dt);
     if (d > 0 && o0 < g1 && g0 < o1) return GAR_ERR_INVALID_ARGUMENT;
   }
   return GAR_OK;
@@ -197,9 +201,11 @@ Workspace carve(void* ws, int n) {
   return w;
 }
 
-gar_status run_gram(const float* const* grads, int n, int64_t d, const Workspace& w, cudaStream_t st) {
+gar_status run_gram(const float* const* grads, int n, int64_t d, const Workspace& w, cudaStream_t st,
+                    gar_dtype dt = GAR_F32) {
   int parts = 0;
-  gar_status s = cuda_status(gar::launch_gram_partials(grads, n, d, w.partials, num_sms(), &parts, st));
+  gar_status s =
+      cuda_status(gar::launch_gram_partials(grads, n, d, w.partials, num_sms(), &parts, st, nullptr, dt));
   if (s != GAR_OK) return s;
   return cuda_status(gar::launch_gram_reduce(w.partials, parts, n, w.G, st));
 }
@@ -217,8 +223,10 @@ gar_status run_select(gar_rule rule, const double* G, int n, int f, int me, int3
 }
 
 gar_status run_combine(gar_rule rule, const float* const* grads, int n, int f, int me, int64_t d,
-                       const int32_t* idx, float* out, const gar::OutPtrs& extra, cudaStream_t st) {
+                       const int32_t* idx, float* out, const gar::OutPtrs& extra, cudaStream_t st,
+                       gar_dtype dt = GAR_F32) {
   CoordLaunch L{};
+  L.dtype = dt;
   L.rows = grads;
   L.n = n;
   L.idx = idx;
@@ -262,11 +270,12 @@ gar_status make_mc(float* out_mc, gar::OutPtrs* extra) {
 
 gar_status aggregate_impl(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d, float* out,
                           const gar::OutPtrs& extra, int32_t* indices_dev, void* workspace, size_t workspace_bytes,
-                          gar_stream_t stream) {
+                          gar_stream_t stream, gar_dtype dt = GAR_F32) {
+  if (!valid_dtype(dt)) return GAR_ERR_INVALID_ARGUMENT;
   gar_status s = check_rule_args(rule, n, f, m);
   if (s != GAR_OK) return s;
   if ((s = check_rows(grads, n, d)) != GAR_OK) return s;
-  if ((s = check_out(grads, n, d, out)) != GAR_OK) return s;
+  if ((s = check_out(grads, n, d, out, dt)) != GAR_OK) return s;
   const bool krum = is_krum_family(rule);
   if (krum && (!workspace || workspace_bytes < ws_bytes_for(n))) return GAR_ERR_WORKSPACE;
   if ((s = check_device_rows(grads, n, out)) != GAR_OK) return s;
@@ -274,6 +283,7 @@ gar_status aggregate_impl(gar_rule rule, const float* const* grads, int n, int f
 
   if (!krum) {
     CoordLaunch L{};
+    L.dtype = dt;
     L.rows = grads;
     L.n = n;
     L.idx = nullptr;
@@ -293,22 +303,83 @@ gar_status aggregate_impl(gar_rule rule, const float* const* grads, int n, int f
   const int me = effective_m(rule, n, f, m);
   Workspace w = carve(workspace, n);
   int32_t* idx = indices_dev ? indices_dev : w.idx;
-  if ((s = run_gram(grads, n, d, w, st)) != GAR_OK) return s;
+  if ((s = run_gram(grads, n, d, w, st, dt)) != GAR_OK) return s;
   if ((s = run_select(rule, w.G, n, f, me, idx, nullptr, &w, st)) != GAR_OK) return s;
-  return run_combine(rule, grads, n, f, me, d, idx, out, extra, st);
+  return run_combine(rule, grads, n, f, me, d, idx, out, extra, st, dt);
 }
 
 gar_status combine_impl(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d_local,
-                        const int32_t* indices_dev, float* out, const gar::OutPtrs& extra, gar_stream_t stream) {
+                        const int32_t* indices_dev, float* out, const gar::OutPtrs& extra, gar_stream_t stream,
+                        gar_dtype dt = GAR_F32) {
+  if (!valid_dtype(dt)) return GAR_ERR_INVALID_ARGUMENT;
   gar_status s = check_rule_args(rule, n, f, m);
   if (s != GAR_OK) return s;
   if (!is_krum_family(rule)) return GAR_ERR_UNSUPPORTED;
   if (!indices_dev) return GAR_ERR_INVALID_ARGUMENT;
   if ((s = check_rows(grads, n, d_local)) != GAR_OK) return s;
-  if ((s = check_out(grads, n, d_local, out)) != GAR_OK) return s;
+  if ((s = check_out(grads, n, d_local, out, dt)) != GAR_OK) return s;
   if ((s = check_device_rows(grads, n, out)) != GAR_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  return run_combine(rule, grads, n, f, effective_m(rule, n, f, m), d_local, indices_dev, out, extra, st);
+  return run_combine(rule, grads, n, f, effective_m(rule, n, f, m), d_local, indices_dev, out, extra, st, dt);
+}
+
+gar_status select_impl(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d,
+                       int32_t* indices_dev, int* n_selected_host, void* workspace, size_t workspace_bytes,
+                       gar_stream_t stream, gar_dtype dt) {
+  if (!valid_dtype(dt)) return GAR_ERR_INVALID_ARGUMENT;
+  gar_status s = check_rule_args(rule, n, f, m);
+  if (s != GAR_OK) return s;
+  if (!is_krum_family(rule)) return GAR_ERR_UNSUPPORTED;
+  if (!indices_dev) return GAR_ERR_INVALID_ARGUMENT;
+  if ((s = check_rows(grads, n, d)) != GAR_OK) return s;
+  if (!workspace || workspace_bytes < ws_bytes_for(n)) return GAR_ERR_WORKSPACE;
+  if ((s = check_device_rows(grads, n, nullptr)) != GAR_OK) return s;
+  if ((s = check_device_ptr(indices_dev)) != GAR_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int me = effective_m(rule, n, f, m);
+  Workspace w = carve(workspace, n);
+  if ((s = run_gram(grads, n, d, w, st, dt)) != GAR_OK) return s;
+  if ((s = run_select(rule, w.G, n, f, me, indices_dev, nullptr, &w, st)) != GAR_OK) return s;
+  if (n_selected_host) *n_selected_host = gar_num_selected(rule, n, f, m);
+  return GAR_OK;
+}
+
+gar_status distances_impl(const float* const* grads, int n, int64_t d, double* D_dev, void* workspace,
+                          size_t workspace_bytes, gar_stream_t stream, gar_dtype dt) {
+  if (!valid_dtype(dt)) return GAR_ERR_INVALID_ARGUMENT;
+  if (n < 1 || n > GAR_MAX_N || !D_dev) return GAR_ERR_INVALID_ARGUMENT;
+  gar_status s = check_rows(grads, n, d);
+  if (s != GAR_OK) return s;
+  if (!workspace || workspace_bytes < ws_bytes_for(n)) return GAR_ERR_WORKSPACE;
+  if ((s = check_device_rows(grads, n, nullptr)) != GAR_OK) return s;
+  if ((s = check_device_ptr(D_dev)) != GAR_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace w = carve(workspace, n);
+  if ((s = run_gram(grads, n, d, w, st, dt)) != GAR_OK) return s;
+  return cuda_status(gar::launch_select(w.G, n, 0, 0, gar::kSelDistancesOnly, w.idx, D_dev, st));
+}
+
+gar_status gram_partial_impl(const float* const* grads, int n, int64_t d_local, double* gram_dev, void* workspace,
+                             size_t workspace_bytes, gar_stream_t stream, gar_dtype dt) {
+  if (!valid_dtype(dt)) return GAR_ERR_INVALID_ARGUMENT;
+  if (n < 1 || n > GAR_MAX_N || !gram_dev) return GAR_ERR_INVALID_ARGUMENT;
+  gar_status s = check_rows(grads, n, d_local);
+  if (s != GAR_OK) return s;
+  if (!workspace || workspace_bytes < ws_bytes_for(n)) return GAR_ERR_WORKSPACE;
+  if ((s = check_device_rows(grads, n, nullptr)) != GAR_OK) return s;
+  if ((s = check_device_ptr(gram_dev)) != GAR_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace w = carve(workspace, n);
+  int parts = 0;
+  if ((s = cuda_status(gar::launch_gram_partials(grads, n, d_local, w.partials, num_sms(), &parts, st, nullptr,
+                                                 dt))) != GAR_OK)
+    return s;
+  return cuda_status(gar::launch_gram_reduce(w.partials, parts, n, gram_dev, st));
+}
+
+// the bf16 entry points take the rows as untyped pointers
+inline const float* const* rows_cast(const void* const* grads) {
+  return reinterpret_cast<const float* const*>(grads);
 }
 
 }  // namespace
@@ -382,51 +453,18 @@ gar_status gar_aggregate(gar_rule rule, const float* const* grads, int n, int f,
 gar_status gar_select(gar_rule rule, const float* const* grads, int n, int f, int m, int64_t d,
                       int32_t* indices_dev, int* n_selected_host, void* workspace, size_t workspace_bytes,
                       gar_stream_t stream) {
-  gar_status s = check_rule_args(rule, n, f, m);
-  if (s != GAR_OK) return s;
-  if (!is_krum_family(rule)) return GAR_ERR_UNSUPPORTED;
-  if (!indices_dev) return GAR_ERR_INVALID_ARGUMENT;
-  if ((s = check_rows(grads, n, d)) != GAR_OK) return s;
-  if (!workspace || workspace_bytes < ws_bytes_for(n)) return GAR_ERR_WORKSPACE;
-  if ((s = check_device_rows(grads, n, nullptr)) != GAR_OK) return s;
-  if ((s = check_device_ptr(indices_dev)) != GAR_OK) return s;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int me = effective_m(rule, n, f, m);
-  Workspace w = carve(workspace, n);
-  if ((s = run_gram(grads, n, d, w, st)) != GAR_OK) return s;
-  if ((s = run_select(rule, w.G, n, f, me, indices_dev, nullptr, &w, st)) != GAR_OK) return s;
-  if (n_selected_host) *n_selected_host = gar_num_selected(rule, n, f, m);
-  return GAR_OK;
+  return select_impl(rule, grads, n, f, m, d, indices_dev, n_selected_host, workspace, workspace_bytes, stream,
+                     GAR_F32);
 }
 
 gar_status gar_distances(const float* const* grads, int n, int64_t d, double* D_dev, void* workspace,
                          size_t workspace_bytes, gar_stream_t stream) {
-  if (n < 1 || n > GAR_MAX_N || !D_dev) return GAR_ERR_INVALID_ARGUMENT;
-  gar_status s = check_rows(grads, n, d);
-  if (s != GAR_OK) return s;
-  if (!workspace || workspace_bytes < ws_bytes_for(n)) return GAR_ERR_WORKSPACE;
-  if ((s = check_device_rows(grads, n, nullptr)) != GAR_OK) return s;
-  if ((s = check_device_ptr(D_dev)) != GAR_OK) return s;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  Workspace w = carve(workspace, n);
-  if ((s = run_gram(grads, n, d, w, st)) != GAR_OK) return s;
-  return cuda_status(gar::launch_select(w.G, n, 0, 0, gar::kSelDistancesOnly, w.idx, D_dev, st));
+  return distances_impl(grads, n, d, D_dev, workspace, workspace_bytes, stream, GAR_F32);
 }
 
 gar_status gar_gram_partial(const float* const* grads, int n, int64_t d_local, double* gram_dev, void* workspace,
                             size_t workspace_bytes, gar_stream_t stream) {
-  if (n < 1 || n > GAR_MAX_N || !gram_dev) return GAR_ERR_INVALID_ARGUMENT;
-  gar_status s = check_rows(grads, n, d_local);
-  if (s != GAR_OK) return s;
-  if (!workspace || workspace_bytes < ws_bytes_for(n)) return GAR_ERR_WORKSPACE;
-  if ((s = check_device_rows(grads, n, nullptr)) != GAR_OK) return s;
-  if ((s = check_device_ptr(gram_dev)) != GAR_OK) return s;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  Workspace w = carve(workspace, n);
-  int parts = 0;
-  if ((s = cuda_status(gar::launch_gram_partials(grads, n, d_local, w.partials, num_sms(), &parts, st))) != GAR_OK)
-    return s;
-  return cuda_status(gar::launch_gram_reduce(w.partials, parts, n, gram_dev, st));
+  return gram_partial_impl(grads, n, d_local, gram_dev, workspace, workspace_bytes, stream, GAR_F32);
 }
 
 gar_status gar_select_from_gram(gar_rule rule, const double* gram_dev, int n, int f, int m, int32_t* indices_dev,
@@ -554,6 +592,38 @@ gar_status gar_trimmed_membership(const float* const* grads, int n, int f, int64
   if ((s = check_device_rows(grads, n, mask_dev)) != GAR_OK) return s;
   return cuda_status(gar::launch_trimmed_membership(grads, n, f, d, mask_dev, num_sms(),
                                                     reinterpret_cast<cudaStream_t>(stream)));
+}
+
+// ---- bf16 gradient rows (R16) -------------------
+gar_status gar_aggregate_dt(gar_rule rule, gar_dtype dtype, const void* const* grads, int n, int f, int m, int64_t d,
+                            float* out, int32_t* indices_dev, void* workspace, size_t workspace_bytes,
+                            gar_stream_t stream) {
+  gar::OutPtrs none{};
+  return aggregate_impl(rule, rows_cast(grads), n, f, m, d, out, none, indices_dev, workspace, workspace_bytes,
+                        stream, dtype);
+}
+
+gar_status gar_select_dt(gar_rule rule, gar_dtype dtype, const void* const* grads, int n, int f, int m, int64_t d,
+                         int32_t* indices_dev, int* n_selected_host, void* workspace, size_t workspace_bytes,
+                         gar_stream_t stream) {
+  return select_impl(rule, rows_cast(grads), n, f, m, d, indices_dev, n_selected_host, workspace, workspace_bytes,
+                     stream, dtype);
+}
+
+gar_status gar_distances_dt(gar_dtype dtype, const void* const* grads, int n, int64_t d, double* D_dev,
+                            void* workspace, size_t workspace_bytes, gar_stream_t stream) {
+  return distances_impl(rows_cast(grads), n, d, D_dev, workspace, workspace_bytes, stream, dtype);
+}
+
+gar_status gar_gram_partial_dt(gar_dtype dtype, const void* const* grads, int n, int64_t d_local, double* gram_dev,
+                               void* workspace, size_t workspace_bytes, gar_stream_t stream) {
+  return gram_partial_impl(rows_cast(grads), n, d_local, gram_dev, workspace, workspace_bytes, stream, dtype);
+}
+
+gar_status gar_combine_dt(gar_rule rule, gar_dtype dtype, const void* const* grads, int n, int f, int m,
+                          int64_t d_local, const int32_t* indices_dev, float* out, gar_stream_t stream) {
+  gar::OutPtrs none{};
+  return combine_impl(rule, rows_cast(grads), n, f, m, d_local, indices_dev, out, none, stream, dtype);
 }
 
 }  // extern "C"

@@ -10,7 +10,9 @@ relabel), and Batcher's merge exchange on exactly N wires.  Only the min/max
 outputs that reach the requested output positions are kept, and the cheapest
 construction (in emitted min/max instructions) wins per (N, outputs).
 
-Emitted functions (all in-place on ``float v[N]``, ascending order):
+Emitted functions (all in-place on ``T v[N]``, ascending order; T = float, or
+``bf2`` = two bf16 values of adjacent coordinates in one 32-bit register, whose
+compare-exchange is one packed min.bf16x2 / max.NaN.bf16x2 pair — elem.cuh):
 
 * ``gar_net::sort_<N>(v)``    — full sort, every position valid;
 * ``gar_net::median_<N>(v)``  — only v[(N-1)/2] (and v[N/2] for even N) valid;
@@ -19,8 +21,8 @@ Emitted functions (all in-place on ``float v[N]``, ascending order):
 * ``gar_net::window_<N>(v)``  — odd N >= 5: v[h-2..h+2] valid and sorted,
   h = (N-1)/2: Bulyan's coordinate phase when beta = 3 (n = 4f+3).
 
-Compare-exchange = fminf (FMNMX, drops a NaN operand) + max_nan (FMNMX.NAN,
-returns NaN if either operand is NaN).  With these two, a NaN moves through
+Compare-exchange = vmin (fminf / min.bf16x2: drops a NaN operand) + vmax_nan
+(max.NaN: returns NaN if either operand is NaN).  With these two, a NaN moves through
 the network exactly like +inf (R1: NaN orders as +inf): min(NaN, x) = x,
 max(NaN, x) = NaN, min/max(NaN, NaN) = NaN.  So inputs need no
 canonicalisation; the kernel maps NaN -> +inf only on the outputs it uses.
@@ -217,7 +219,7 @@ def emit(N, fname, positions):
     if len(positions) == N and N <= 2:
         what = "full sort"
     lines = [f"// N={N}: {name}, {cost} min/max ({what})",
-             f"__device__ __forceinline__ void {fname}_{N}(float* v) {{"]
+             f"template <class T> __device__ __forceinline__ void {fname}_{N}(T* v) {{"]
     names = {}
 
     def ref(x):
@@ -226,14 +228,14 @@ def emit(N, fname, positions):
         return names[x[1]]
 
     for i in range(N):
-        lines.append(f"  const float v{i} = v[{i}];")
+        lines.append(f"  const T v{i} = v[{i}];")
     for k, (kind, a, b) in enumerate(ops):
         if k not in live:
             continue
         nm = f"t{k}"
         names[k] = nm
-        fn = "fminf" if kind == "min" else "max_nan"
-        lines.append(f"  const float {nm} = {fn}({ref(a)}, {ref(b)});")
+        fn = "vmin" if kind == "min" else "vmax_nan"
+        lines.append(f"  const T {nm} = {fn}({ref(a)}, {ref(b)});")
     for p in positions:
         lines.append(f"  v[{p}] = {ref(final[p])};")
     lines.append("}")
@@ -249,13 +251,8 @@ def main(out_path):
              "// shares nothing with oracle/.  Pruned Batcher / bitonic / pairwise /",
              "// merge-exchange networks with +inf padding constant-propagated",
              "// (DESIGN.md §4.1, coord_select).",
-             "#pragma once", "namespace gar_net {",
-             "// NaN-propagating max (PTX max.NaN): NaN behaves as +inf in the networks.",
-             "__device__ __forceinline__ float max_nan(float a, float b) {",
-             "  float r;",
-             "  asm(\"max.NaN.f32 %0, %1, %2;\" : \"=f\"(r) : \"f\"(a), \"f\"(b));",
-             "  return r;",
-             "}"]
+             "#pragma once", "#include \"elem.cuh\"", "namespace gar_net {",
+             "using gar::vmin;", "using gar::vmax_nan;"]
     table = []
     for N in range(1, MAXN + 1):
         src, c_sort = emit(N, "sort", list(range(N)))
@@ -271,17 +268,18 @@ def main(out_path):
             src, _ = emit(N, "window", list(range(h - 2, h + 3)))
             parts.append(src)
         table.append((N, c_sort, c_med, c_trim))
-    parts.append("template <int N> __device__ __forceinline__ void sort_net(float* v);")
-    parts.append("template <int N> __device__ __forceinline__ void trim_net(float* v);")
-    parts.append("template <int N> __device__ __forceinline__ void window_net(float* v);")
     parts.append("template <int N> constexpr int trim_f() { return N >= 3 ? (N - 3) / 4 : 0; }")
-    parts.append("template <int N> __device__ __forceinline__ void median_net(float* v);")
+    parts.append("template <int N> struct Net;")
     for N in range(1, MAXN + 1):
-        parts.append(f"template <> __device__ __forceinline__ void sort_net<{N}>(float* v) {{ sort_{N}(v); }}")
-        parts.append(f"template <> __device__ __forceinline__ void median_net<{N}>(float* v) {{ median_{N}(v); }}")
-        parts.append(f"template <> __device__ __forceinline__ void trim_net<{N}>(float* v) {{ trim_{N}(v); }}")
+        body = (f"template <> struct Net<{N}> {{ "
+                f"template <class T> static __device__ __forceinline__ void sort(T* v) {{ sort_{N}(v); }} "
+                f"template <class T> static __device__ __forceinline__ void median(T* v) {{ median_{N}(v); }} "
+                f"template <class T> static __device__ __forceinline__ void trim(T* v) {{ trim_{N}(v); }}")
         if N % 2 == 1 and N >= 5:
-            parts.append(f"template <> __device__ __forceinline__ void window_net<{N}>(float* v) {{ window_{N}(v); }}")
+            body += f" template <class T> static __device__ __forceinline__ void window(T* v) {{ window_{N}(v); }}"
+        parts.append(body + " };")
+    for k in ("sort", "median", "trim", "window"):
+        parts.append(f"template <int N, class T> __device__ __forceinline__ void {k}_net(T* v) {{ Net<N>::{k}(v); }}")
     parts.append("// min/max instruction counts (N, sort, median, trim at F = trim_f<N>):")
     for N, a, b, c in table:
         parts.append(f"//   {N:2d} {a:4d} {b:4d} {c:4d}")

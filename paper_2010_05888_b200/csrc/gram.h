@@ -22,7 +22,7 @@ constexpr int kGramMaxParts = 160;
 // there from the kernel's staging ring (fused ingress staging).
 cudaError_t launch_gram_partials(const float* const* rows, int n, int64_t d, double* partials,
                                  int num_sms, int* n_parts, cudaStream_t stream,
-                                 float* const* stage_rows = nullptr);
+                                 float* const* stage_rows = nullptr, int dtype = 0 /* ElemType */);
 
 // G = sum_p partials[p] in fixed order p = 0..n_parts-1 (deterministic).
 cudaError_t launch_gram_reduce(const double* partials, int n_parts, int n, double* G,

@@ -56,8 +56,17 @@ def shard_len(d: int, world: int, align: int = 1024) -> int:
     return shard_bounds(d, 0, world, align)[1] if world > 1 else d
 
 
+def is_bf16(rows) -> bool:
+    """bf16 gradient rows: a bf16 tensor or a list of them."""
+    t = rows if isinstance(rows, torch.Tensor) else (rows[0] if isinstance(rows, (list, tuple)) and rows else None)
+    return t is not None and t.dtype == torch.bfloat16
+
+
 class _LibgarBackend:
-    """The product kernels (libgar C ABI)."""
+    """The product kernels (libgar C ABI).  bf16 rows go through the _dt entry
+    points (exact widening, R16); the peer-memory exchange and the
+    fused outputs are fp32-only, so bf16 rows use the NCCL exchange and a
+    separate all-gather."""
 
     def __init__(self):
         from . import _lib
@@ -67,7 +76,10 @@ class _LibgarBackend:
         agg.aggregate(rows, out=out, d=d)
 
     def gram_partial(self, rows, gram, ws, d):
-        self._lib.gar_gram_partial(rows, gram, ws, d=d)
+        if is_bf16(rows):
+            self._lib.gar_gram_partial_dt(rows, gram, ws, d=d)
+        else:
+            self._lib.gar_gram_partial(rows, gram, ws, d=d)
 
     def select_from_gram(self, rule, gram, n, f, m, idx, ws=None):
         return self._lib.gar_select_from_gram(rule, gram, n, f, m, idx, workspace=ws)
@@ -76,7 +88,11 @@ class _LibgarBackend:
         self._lib.gar_gram_exchange(rows, gram, ws, slots, flags, rank, world, epoch, d=d, stage=stage)
 
     def combine(self, rule, rows, f, m, idx, out, d, extra=()):
-        if isinstance(extra, Multicast):
+        if is_bf16(rows):
+            if extra:
+                raise NotImplementedError("fused outputs take fp32 rows; use output='replicated' for bf16")
+            self._lib.gar_combine_dt(rule, rows, f, m, idx, out, d=d)
+        elif isinstance(extra, Multicast):
             self._lib.gar_combine_mcast(rule, rows, f, m, idx, out, extra.addr, d=d)
         elif extra:
             self._lib.gar_combine_bcast(rule, rows, f, m, idx, out, extra, d=d)
@@ -174,8 +190,10 @@ class ShardedAggregator:
             self._stage = torch.empty((self.n, ld), dtype=torch.float32, device=dev)
         return self._stage
 
-    def _use_peer_exchange(self, device) -> bool:
+    def _use_peer_exchange(self, device, rows=None) -> bool:
         if self.world <= 1 or self.rule not in KRUM_FAMILY or device.type != "cuda":
+            return False
+        if rows is not None and is_bf16(rows):
             return False
         if self.exchange == "nccl" or not hasattr(self.backend, "gram_exchange"):
             return False
@@ -202,7 +220,7 @@ class ShardedAggregator:
     def _gram_whole(self, rows_local, dev, mark, stage=None):
         """Whole-vector Gram matrix on every rank (self._gram); with `stage`
         the Gram kernel also copies the rows there (fused ingress staging)."""
-        if self._use_peer_exchange(dev):
+        if self._use_peer_exchange(dev, rows_local):
             x = self._exchange_buffers(dev)
             x["epoch"] += 1
             par = x["epoch"] % 2

@@ -55,17 +55,22 @@ class Aggregator:
 
     def aggregate(self, grads, out: torch.Tensor | None = None, d: int | None = None,
                   indices: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-        """out (fp32[d]) = GAR(grads); grads: list of n CUDA fp32 vectors or an [n, ld] matrix."""
+        """out (fp32[d]) = GAR(grads); grads: list of n CUDA fp32 (or bf16) vectors or an
+        [n, ld] matrix.  bf16 inputs are widened exactly to fp32 (R16)."""
         self._check_n(grads)
-        arr, n, d, dev = _lib.row_pointers(grads, d)
+        arr, n, d, dev, dt = _lib.row_pointers_dt(grads, d)
         if out is None:
             out = torch.empty(d, dtype=torch.float32, device=dev)
         ws = self.workspace(dev)
         wsb = 0 if ws is None else ws.numel()
         o = _lib._buf(out, torch.float32, d, dev, "out")
         ix = _lib._idx(indices, self.rule, n, self.f, self.m, dev, True)
-        _lib.check(_lib.lib.gar_aggregate_ex(self.rid, arr, n, self.f, self.m, d, o, ix, _lib._ptr(ws), wsb,
-                                             _lib.stream_handle(dev, stream)), f"aggregate[{self.rule}]")
+        if dt == 0:
+            _lib.check(_lib.lib.gar_aggregate_ex(self.rid, arr, n, self.f, self.m, d, o, ix, _lib._ptr(ws), wsb,
+                                                 _lib.stream_handle(dev, stream)), f"aggregate[{self.rule}]")
+        else:
+            _lib.check(_lib.lib.gar_aggregate_dt(self.rid, dt, arr, n, self.f, self.m, d, o, ix, _lib._ptr(ws), wsb,
+                                                 _lib.stream_handle(dev, stream)), f"aggregate[{self.rule}]")
         return out
 
     def graphed(self, grads, out: torch.Tensor, d: int | None = None, indices: torch.Tensor | None = None):
@@ -91,12 +96,13 @@ class Aggregator:
     def select(self, grads, d: int | None = None, stream=None) -> torch.Tensor:
         """Selected input indices (device int32), in selection order."""
         self._check_n(grads)
-        arr, n, d, dev = _lib.row_pointers(grads, d)
+        arr, n, d, dev, dt = _lib.row_pointers_dt(grads, d)
         ws = self.workspace(dev)
         if ws is None:
             raise _lib.GarError(5, f"select[{self.rule}]")
         idx = torch.empty(_lib.MAX_N, dtype=torch.int32, device=dev)
-        nsel = _lib.gar_select(self.rule, grads, self.f, self.m, idx, ws, d=d, stream=stream)
+        sel = _lib.gar_select if dt == 0 else _lib.gar_select_dt
+        nsel = sel(self.rule, grads, self.f, self.m, idx, ws, d=d, stream=stream)
         return idx[:nsel]
 
 

@@ -106,6 +106,18 @@ def make_gradients(n: int, f: int, d: int, seed: int, kind: str = "byzantine",
     return x
 
 
+def to_bf16(x: torch.Tensor) -> torch.Tensor:
+    """bf16 copy of a generated fp32 matrix (torch's round-to-nearest-even
+    conversion), for the bf16-input variant.  Input generation
+    only: both sides receive these bf16 bits."""
+    return x.to(torch.bfloat16)
+
+
+def bf16_bits(x: torch.Tensor) -> np.ndarray:
+    """The uint16 bit patterns of a bf16 tensor (what the oracle takes)."""
+    return x.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16)
+
+
 def make_sharded_gradients(n: int, f: int, d: int, seed: int, rank: int, world: int,
                            device="cpu", kind: str = "byzantine") -> tuple[torch.Tensor, int, int]:
     """d-sharded view for rank ``rank``: rows restricted to its coordinate slice.

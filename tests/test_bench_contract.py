@@ -59,3 +59,19 @@ def test_our_arm_line():
     assert e["value"] > 0 and n * d * 4 <= e["h2d_bytes_per_step"] < n * (d + 64) * 4
     assert 6 * d * 4 <= e["d2h_bytes_per_step"] < 6 * (d + 64) * 4
     assert j["gpu_launches"] > 0 and set(j["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    v = j["variants"]["bf16"]                # the bf16 variant of the same step
+    assert v["value"] > 0 and v["ms_per_step"] > 0 and set(v["per_rule"]) == set(j["per_rule"])
+
+
+@pytest.mark.gpu
+def test_our_arm_line_bf16():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    j = _run("--workload", "C1", "--steps", "3", "--warmup", "3", "--e2e-steps", "2", "--dtype", "bf16")
+    _check_common(j, 3, 3)
+    assert j["dtype"] == "bf16" and "bf16" in j["metric"]
+    n, d = j["config"]["n"], j["config"]["d"]
+    e = j["e2e"]
+    assert n * d * 2 <= e["h2d_bytes_per_step"] < n * (d + 64) * 2
+    assert j["roofline"]["frac"] > 0

@@ -517,3 +517,61 @@ def test_sanitize_spec_examples():
     assert oracle.sanitize(np.array([[1, 2], [nan, 4], [5, 6]], np.float32), 1) == ([0, 2], [1])
     with pytest.raises(oracle.OracleError):
         oracle.sanitize(np.array([[nan, 1], [1, inf]], np.float32), 1)
+
+
+# ---- bf16 inputs (R16) ------------------------------
+# bf16 is the upper half of IEEE-754 binary32: sign, 8-bit exponent, 7 fraction
+# bits.  These values follow from that definition alone.
+BF16_GOLDEN = [
+    (0x3F80, 1.0), (0xBF80, -1.0), (0x4000, 2.0), (0x4049, 3.140625), (0x3DCD, 0.10009765625),
+    (0x0000, 0.0), (0x7F80, math.inf), (0xFF80, -math.inf),
+    (0x0001, 2.0 ** -133),                 # smallest subnormal: 2^-126 * 2^-7
+    (0x0080, 2.0 ** -126),                 # smallest normal
+    (0x7F7F, (2.0 - 2.0 ** -7) * 2.0 ** 127),   # largest finite
+    (0xC2C8, -100.0),
+]
+
+
+def test_widen_bf16_golden():
+    bits = np.array([b for b, _ in BF16_GOLDEN], np.uint16)
+    got = oracle.widen_bf16(bits)
+    assert got.dtype == np.float32
+    for (b, v), g in zip(BF16_GOLDEN, got):
+        assert float(g) == v, hex(b)
+    neg0 = oracle.widen_bf16(np.array([0x8000], np.uint16))[0]
+    assert neg0 == 0.0 and math.copysign(1.0, float(neg0)) < 0
+    assert np.isnan(oracle.widen_bf16(np.array([0x7FC0, 0xFFC1, 0x7F81], np.uint16))).all()
+
+
+def test_widen_bf16_matches_torch_on_every_pattern():
+    """All 65536 patterns against torch's own bfloat16 -> float32 conversion
+    (an independent library routine)."""
+    import torch
+    bits = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    ours = oracle.widen_bf16(bits)
+    ref = torch.from_numpy(bits.view(np.int16).copy()).view(torch.bfloat16).float().numpy()
+    same = (ours.view(np.uint32) == ref.view(np.uint32)) | (np.isnan(ours) & np.isnan(ref))
+    assert same.all()
+
+
+def test_bf16_rules_are_the_fp32_rules_on_widened_values():
+    """R16 end to end on a small case, against the brute forces: the median of
+    bf16 inputs is itself a bf16 value (low 16 bits zero), and every rule
+    equals the brute-force fp32 rule of the widened matrix."""
+    rng = np.random.default_rng(15)
+    n, f, d = 11, 2, 6
+    x32 = (rng.standard_normal((n, d)) * 0.01).astype(np.float32)
+    bits = (x32.view(np.uint32) >> 16).astype(np.uint16)           # truncation: any bf16 pattern will do
+    bits[3, 2] = 0x7FC0                                             # a NaN payload
+    bits[5, 4] = 0x8000                                             # -0
+    xw = oracle.widen_bf16(bits)
+    med = oracle.aggregate_bf16("median", bits, f)[0]
+    assert (med.view(np.uint32) & 0xFFFF == 0).all()
+    np.testing.assert_array_equal(med, np.array([brute.median(xw[:, k:k + 1], f)[0] for k in range(d)], np.float32))
+    tm = oracle.aggregate_bf16("trimmed_mean", bits, f)[0]
+    np.testing.assert_array_equal(tm, np.array([brute.trimmed_mean(xw[:, k:k + 1], f)[0] for k in range(d)],
+                                               np.float32))
+    out, sel = oracle.aggregate_bf16("bulyan", bits[:, [0, 1, 3, 5]], f)   # finite columns only
+    bo, bs = brute.bulyan(xw[:, [0, 1, 3, 5]], f)
+    np.testing.assert_array_equal(sel, bs)
+    np.testing.assert_array_equal(out, bo)
