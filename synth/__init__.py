@@ -109,7 +109,12 @@ def make_gradients(n: int, f: int, d: int, seed: int, kind: str = "byzantine",
 def to_bf16(x: torch.Tensor) -> torch.Tensor:
     """bf16 copy of a generated fp32 matrix (torch's round-to-nearest-even
     conversion), for the bf16-input variant.  Input generation
-    only: both sides receive these bf16 bits."""
+    only: both sides receive these bf16 bits.  A 2-D matrix keeps 16-byte
+    aligned rows: its row length is padded with zeros to a multiple of 8."""
+    if x.dim() == 2 and x.shape[1] % 8:
+        y = torch.zeros((x.shape[0], (x.shape[1] + 7) // 8 * 8), dtype=torch.bfloat16, device=x.device)
+        y[:, : x.shape[1]] = x
+        return y
     return x.to(torch.bfloat16)
 
 

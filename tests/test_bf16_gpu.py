@@ -35,7 +35,7 @@ def to_device_bf16(bits: np.ndarray) -> torch.Tensor:
 
 def recipe_bits(n, f, d, seed, kind="byzantine"):
     x = synth.make_gradients(n, f, d, seed=seed, ld=d, kind=kind)
-    return synth.bf16_bits(synth.to_bf16(x))
+    return synth.bf16_bits(synth.to_bf16(x))[:, :d]
 
 
 def run(gar, rule, X, d, f, m=None):
