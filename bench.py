@@ -104,10 +104,31 @@ class Clocks:
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
-        time.sleep(0.3)
+        # the sampler must be running before the timed region starts: wait for
+        # its first line (nvidia-smi can take a second to start on a cold box)
+        t_end = time.time() + 5.0
+        while self.proc is not None and time.time() < t_end:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    break
+            except OSError:
+                pass
+            time.sleep(0.05)
+        self._lines0 = self._count()
         return self
 
+    def _count(self):
+        try:
+            with open(self.path) as fh:
+                return sum(1 for _ in fh)
+        except OSError:
+            return 0
+
     def __exit__(self, *a):
+        # keep sampling until at least two samples cover the timed region
+        t_end = time.time() + 2.0
+        while self.proc is not None and self._count() < self._lines0 + 2 and time.time() < t_end:
+            time.sleep(0.05)
         if self.proc:
             self.proc.terminate()
             self.proc.wait()

@@ -31,7 +31,9 @@ namespace gar {
 // stages of 63 rows in shared memory.  Copy size AND the number of issuing
 // warps matter: bulk-copy issue is limited per warp (tools/membench2.cu:
 // 31 rows x 1 KB go 1.3 -> 5.5 TB/s from 1 to 8 issuing warps), so producer
-// warp p issues rows r = p mod kProducers and arms its own stage barrier.
+// warp p issues rows r = p mod kProducers; each arms the stage's one "full"
+// barrier (kProducers arrivals, each with its own expected bytes), so a
+// consumer waits on one barrier per tile.
 constexpr int kProducers = 4;
 // Consumer warps per CTA (one CTA per SM).  The trimmed mean and the Bulyan
 // phase are ALU-bound (FMNMX networks) and gain from more warps to overlap: 24
@@ -135,6 +137,10 @@ __device__ __forceinline__ void median_column(T* v, float* res) {
 
 // fp64 sum of v[F], ..., v[N-F-1] (half h) in ascending order (R2), F a
 // compile-time constant so only the kept values are converted and added.
+// The kept values are summed raw: a NaN among them stands for +inf (R1), and
+// a raw sum is NaN exactly when the canonical one is +inf or NaN, so one
+// fix-up replaces the per-value NaN -> +inf mapping: NaN -> +inf unless the
+// smallest kept value is -inf (then the canonical sum is -inf + inf = NaN).
 template <int N, int F, class T>
 __device__ __forceinline__ double sum_kept(const T* v, int f, int h) {
   if constexpr (2 * F >= N) {
@@ -143,7 +149,8 @@ __device__ __forceinline__ double sum_kept(const T* v, int f, int h) {
     if (f != F) return sum_kept<N, F + 1>(v, f, h);
     double s = 0.0;
 #pragma unroll
-    for (int t = F; t < N - F; ++t) s += static_cast<double>(nan_to_inf(val(v[t], h)));
+    for (int t = F; t < N - F; ++t) s += static_cast<double>(val(v[t], h));
+    if (s != s) s = (val(v[F], h) == -__int_as_float(0x7f800000)) ? s : static_cast<double>(__int_as_float(0x7f800000));
     return s;
   }
 }
@@ -348,8 +355,8 @@ __global__ void __launch_bounds__(32 * (W + kProducers), 1) coord_select_kernel(
   const int R = (N > 0) ? N : p.R;
   const int stages = p.stages;
   T* tiles = reinterpret_cast<T*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + size_t(stages) * R * kTile * sizeof(T));  // [stages][kProducers]
-  uint64_t* empty = full + stages * kProducers;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + size_t(stages) * R * kTile * sizeof(T));  // [stages]
+  uint64_t* empty = full + stages;
   __shared__ const float* rowp[GAR_MAX_N];
   __shared__ int sel_s[GAR_MAX_N];
 
@@ -367,7 +374,7 @@ __global__ void __launch_bounds__(32 * (W + kProducers), 1) coord_select_kernel(
       for (int r = 0; r < R; ++r) rowp[r] = p.rows.p[r];
     }
     for (int s = 0; s < stages; ++s) {
-      for (int q = 0; q < kProducers; ++q) mbar_init(&full[s * kProducers + q], 1);
+      mbar_init(&full[s], kProducers);
       mbar_init(&empty[s], kConsumerWarps);
     }
     fence_mbar_init();
@@ -388,7 +395,7 @@ __global__ void __launch_bounds__(32 * (W + kProducers), 1) coord_select_kernel(
         const int64_t start = tile * kCoords;
         const int cnt = static_cast<int>((d - start < kCoords ? d - start : int64_t(kCoords)));
         const uint32_t bytes = static_cast<uint32_t>(cnt & ~(kBulkAlign - 1)) * ES;
-        uint64_t* bar = &full[stage * kProducers + q];
+        uint64_t* bar = &full[stage];
         mbar_arrive_expect_tx(bar, bytes * my_rows);
         if (bytes) {
           T* dst = tiles + size_t(stage) * R * kTile;
@@ -409,8 +416,7 @@ __global__ void __launch_bounds__(32 * (W + kProducers), 1) coord_select_kernel(
   uint32_t phase = 0;
   const int c = threadIdx.x;
   for (int64_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-#pragma unroll
-    for (int q = 0; q < kProducers; ++q) mbar_wait(&full[stage * kProducers + q], phase);
+    mbar_wait(&full[stage], phase);
     const int64_t start = tile * kCoords;
     const int cnt = static_cast<int>((d - start < kCoords ? d - start : int64_t(kCoords)));
     const int bulk_cnt = cnt & ~(kBulkAlign - 1);
@@ -624,7 +630,7 @@ inline cudaError_t launch_mode_w(const CoordLaunch& L, cudaStream_t stream) {
   p.stages = stages;
   p.l2_hint = l2_evict_first_enabled();
   p.num_tiles = (L.d + kCoords - 1) / kCoords;
-  const size_t smem = stages * stage_bytes + (kProducers + 1) * stages * sizeof(uint64_t);
+  const size_t smem = stages * stage_bytes + 2 * stages * sizeof(uint64_t);
   auto kern = coord_select_kernel<MODE, N, W, T>;
   int occ = 0;
   cudaError_t e = cached_occupancy(kern, kThreads, smem, &occ);

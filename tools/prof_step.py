@@ -7,9 +7,12 @@ import synth
 import paper_2010_05888_b200 as gar
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "C3"
+bf16 = len(sys.argv) > 2 and sys.argv[2] == "bf16"
 cfg = synth.CONFIGS[wl] if not wl.startswith("sweep:") else synth.sweep_config(int(wl.split(":")[1]))
 n, f, d = cfg.n, cfg.f, cfg.d
 X = synth.make_gradients(n, f, d, seed=synth.BASE_SEED + 2, device="cuda")
+if bf16:
+    X = synth.to_bf16(X)
 aggs = {r: gar.init(r, n, f) for r in ("average", "median", "trimmed_mean", "krum", "multi_krum", "bulyan")}
 out = torch.empty(d, device="cuda")
 for rep in range(2):
