@@ -37,6 +37,19 @@
 #ifndef GRAM_EXP
 #define GRAM_EXP 0
 #endif
+// NP = 64 ring geometry (A/B knobs for tools/gram_exp.sh; defaults = product)
+#ifndef GRAM64_OPS
+#define GRAM64_OPS 2
+#endif
+#ifndef GRAM64_RAW_SUB
+#define GRAM64_RAW_SUB 4
+#endif
+#ifndef GRAM64_RAW_STAGES
+#define GRAM64_RAW_STAGES 0
+#endif
+#ifndef GRAM64_PROD
+#define GRAM64_PROD 3
+#endif
 
 namespace gar {
 
@@ -69,19 +82,23 @@ struct Cfg {
   static constexpr int ATOMS = KB / 32;          // 128-byte K atoms per tile
   static constexpr int ATOM_BYTES = M * 128;     // one K atom of A (8-row groups of 1 KB)
   static constexpr int OP_BYTES = ATOMS * ATOM_BYTES;      // one operand stage (A; B aliases its H rows)
-  static constexpr int OP_STAGES = 2;
+  static constexpr int OP_STAGES = (NP == 64) ? GRAM64_OPS : 2;
   // Raw ring: one TMA bulk copy per row covers RAW_SUB tiles (1.5 KB / 1 KB per
   // row), issued by PROD_WARPS warps (rows r = p mod PROD_WARPS, one barrier
   // each): bulk-copy issue is limited per request and per issuing warp
   // (tools/membench.cu, membench2.cu).
-  static constexpr int PROD_WARPS = 3;     // 5 or 7 for NP = 64 measured slower (tools/gram_exp.sh)
-  static constexpr int RAW_SUB = (NP == 8) ? 1 : (NP == 16) ? 2 : (NP == 32) ? 3 : 4;   // 2 / 2 / 1.5 / 1 KB per row
+  static constexpr int PROD_WARPS = (NP == 64) ? GRAM64_PROD : 3;     // 5 or 7 for NP = 64 measured slower (tools/gram_exp.sh)
+  static constexpr int RAW_SUB = (NP == 8) ? 1 : (NP == 16) ? 2 : (NP == 32) ? 3 : GRAM64_RAW_SUB;   // 2 / 2 / 1.5 / 1 KB per row
   static constexpr int RAW_KT = RAW_SUB * KT;    // coordinates per raw stage
   // bytes per raw row (+16: conflict-free LDS.128 per 8-lane phase for fp32
   // and for bf16 at CH >= 2, LDS.64 per 16-lane phase for bf16 at CH = 1)
   static constexpr int RAW_PITCH = RAW_KT * ES + 16;
-  static constexpr int RAW_BYTES = NP * RAW_PITCH;    // one raw stage (TMA destination)
-  static constexpr int RAW_STAGES = (NP == 8) ? 8 : (NP == 16) ? 4 : (NP == 32) ? 3 : 2;
+  // The raw ring holds round_up(n, 8) rows per stage (not NP): its stage count
+  // is chosen at launch to fill the shared memory left by the operand stages,
+  // so fewer rows buy a deeper ring (n = 35: 3 stages instead of 2; n = 19: 4
+  // instead of 3).  Up to RAW_STAGES_MAX stages.
+  static constexpr int RAW_STAGES_MAX = 8;
+  static constexpr int RAW_STAGES_FIXED = GRAM64_RAW_STAGES;   // (A/B knob: 0 = fill the budget)
   // warp roles: converters | producers | epilogue | MMA = 16 warps (128 registers).
   static constexpr int PRODUCER_WARP = CONV_WARPS;
   static constexpr int EPI_WARP0 = CONV_WARPS + PROD_WARPS;
@@ -91,12 +108,13 @@ struct Cfg {
   static constexpr int THREADS = (MMA_WARP + 1) * 32;
   static constexpr int TMEM_COLS = 2 * N;        // double-buffered accumulator
   static constexpr int FLUSH = 2;                // tiles accumulated in TMEM (fp32) per fp64 drain
-  static constexpr int SMEM_BYTES = OP_STAGES * OP_BYTES + RAW_STAGES * RAW_BYTES + 1024 /*align*/ +
-                                    (2 * OP_STAGES + (PROD_WARPS + 1) * RAW_STAGES + 4) * 8 /*barriers*/ + 16;
+  static constexpr int SMEM_BYTES = 227 * 1024;
+  static constexpr int BAR_BYTES = (2 * OP_STAGES + (PROD_WARPS + 1) * RAW_STAGES_MAX + 4) * 8 + 16;
+  static constexpr int RAW_REGION = SMEM_BYTES - 1024 /*align*/ - OP_STAGES * OP_BYTES - BAR_BYTES;
   static_assert(THREADS == 16 * 32, "16 warps");
-  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  static_assert(RAW_REGION >= 2 * NP * RAW_PITCH, "two raw stages of NP rows");
   // the epilogue parks T/B over the (then idle) operand + raw rings
-  static_assert(2 * NP * (NP + 1) * 8 <= OP_STAGES * OP_BYTES + RAW_STAGES * RAW_BYTES, "epilogue T/B parking space");
+  static_assert(2 * NP * (NP + 1) * 8 <= OP_STAGES * OP_BYTES + RAW_REGION, "epilogue T/B parking space");
   static_assert(NP * 128 * 4 + NP * (NP + 1) * 4 + NP * 4 <= OP_STAGES * OP_BYTES, "centre-pick scratch");
   static_assert(M == 128 && KB % 32 == 0, "tile shape");
 };
@@ -106,18 +124,19 @@ struct Cfg {
 template <int NP, bool STAGE, bool BF>
 __global__ void __launch_bounds__(Cfg<NP, BF>::THREADS, 1)
     gram_tc_kernel(const __grid_constant__ RowPtrs rows, int n, int64_t d, int64_t num_tiles,
-                   double* __restrict__ partials, int l2_hint, const __grid_constant__ RowPtrs stage) {
+                   double* __restrict__ partials, int l2_hint, const __grid_constant__ RowPtrs stage,
+                   int raw_stages, int raw_bytes) {
   using C = Cfg<NP, BF>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment (SWIZZLE_128B) by offsetting the shared array itself, so
   // the compiler keeps the shared address space (LDS/STS, not generic LD/ST)
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* ops = base;                                        // OP_STAGES x A operand (SW128)
-  unsigned char* raw = base + C::OP_STAGES * C::OP_BYTES;           // RAW_STAGES x [NP][RAW_PITCH]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(raw + C::RAW_STAGES * C::RAW_BYTES);
-  uint64_t* raw_full = bars;                          // [RAW_STAGES][PROD_WARPS] TMA bytes landed
-  uint64_t* raw_empty = raw_full + C::RAW_STAGES * C::PROD_WARPS;   // [RAW_STAGES] converters done
-  uint64_t* op_full = raw_empty + C::RAW_STAGES;      // [OP_STAGES] operand written
+  unsigned char* raw = base + C::OP_STAGES * C::OP_BYTES;           // raw_stages x [round_up(n, 8)][RAW_PITCH]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(raw + C::RAW_REGION);
+  uint64_t* raw_full = bars;                          // [RAW_STAGES_MAX][PROD_WARPS] TMA bytes landed
+  uint64_t* raw_empty = raw_full + C::RAW_STAGES_MAX * C::PROD_WARPS;   // [RAW_STAGES_MAX] converters done
+  uint64_t* op_full = raw_empty + C::RAW_STAGES_MAX;  // [OP_STAGES] operand written
   uint64_t* op_free = op_full + C::OP_STAGES;         // [OP_STAGES] MMAs done reading
   uint64_t* acc_full = op_free + C::OP_STAGES;        // [2]
   uint64_t* acc_empty = acc_full + 2;                 // [2]
@@ -130,7 +149,7 @@ __global__ void __launch_bounds__(Cfg<NP, BF>::THREADS, 1)
   const int64_t T = num_tiles * (blockIdx.x + 1) / G - t0;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::RAW_STAGES; ++s) {
+    for (int s = 0; s < raw_stages; ++s) {
       for (int q = 0; q < C::PROD_WARPS; ++q) mbar_init(&raw_full[s * C::PROD_WARPS + q], 1);
       mbar_init(&raw_empty[s], C::CONV_WARPS);
     }
@@ -165,9 +184,11 @@ __global__ void __launch_bounds__(Cfg<NP, BF>::THREADS, 1)
       const int my_rows = (n > q) ? (n - q + C::PROD_WARPS - 1) / C::PROD_WARPS : 0;
       const int64_t k_end = ((t0 + T) * C::KT < d) ? (t0 + T) * C::KT : d;
       const int64_t R = (T + C::RAW_SUB - 1) / C::RAW_SUB;
-      for (int64_t j = 0; j < R; ++j) {
-        const int rs = static_cast<int>(j % C::RAW_STAGES);
-        const uint32_t use = static_cast<uint32_t>(j / C::RAW_STAGES);
+      // ring slot rs and its reuse count, advanced incrementally (the stage
+      // count is a launch parameter: no runtime division in the loop)
+      int rs = 0;
+      uint32_t use = 0;
+      for (int64_t j = 0; j < R; ++j, (++rs == raw_stages) ? (rs = 0, ++use) : 0) {
         if (use > 0) mbar_wait_sleep(&raw_empty[rs], (use - 1) & 1);
         const int64_t k0 = t0 * C::KT + j * C::RAW_KT;
         const int64_t cnt = (k_end - k0 < C::RAW_KT) ? k_end - k0 : C::RAW_KT;
@@ -175,7 +196,7 @@ __global__ void __launch_bounds__(Cfg<NP, BF>::THREADS, 1)
         uint64_t* bar = &raw_full[rs * C::PROD_WARPS + q];
         mbar_arrive_expect_tx(bar, bytes * static_cast<uint32_t>(my_rows));
         if (bytes) {
-          unsigned char* dst = raw + rs * C::RAW_BYTES;
+          unsigned char* dst = raw + rs * raw_bytes;
           for (int r = q; r < n; r += C::PROD_WARPS) {
             const void* src = reinterpret_cast<const unsigned char*>(rows.p[r]) + k0 * C::ES;
             if (l2_hint) bulk_g2s(dst + r * C::RAW_PITCH, src, bytes, bar, pol);
@@ -224,11 +245,11 @@ __global__ void __launch_bounds__(Cfg<NP, BF>::THREADS, 1)
     const unsigned char* raw_me = raw + Q[0] * CB + g * C::RAW_PITCH;   // chunks Q[0], Q[0]+1, ... are adjacent
     const unsigned char* raw_c = raw + Q[0] * CB + rc * C::RAW_PITCH;
     const int64_t R = (T + C::RAW_SUB - 1) / C::RAW_SUB;
-    for (int64_t j = 0; j < R; ++j) {
-      const int rs = static_cast<int>(j % C::RAW_STAGES);
+    int rs = 0;
+    uint32_t rphase = 0;
+    for (int64_t j = 0; j < R; ++j, (++rs == raw_stages) ? (rs = 0, rphase ^= 1) : 0) {
 #pragma unroll
-      for (int q = 0; q < C::PROD_WARPS; ++q)
-        mbar_wait(&raw_full[rs * C::PROD_WARPS + q], static_cast<uint32_t>(j / C::RAW_STAGES) & 1);
+      for (int q = 0; q < C::PROD_WARPS; ++q) mbar_wait(&raw_full[rs * C::PROD_WARPS + q], rphase);
       // fused ingress staging (gar_gram_exchange with stage rows): the landed
       // raw stage -- rows that may live on other GPUs -- is also written to
       // this GPU's stage buffers by bulk stores, so the combine that follows
@@ -242,7 +263,7 @@ __global__ void __launch_bounds__(Cfg<NP, BF>::THREADS, 1)
         if (bytes) {
           for (int r = 0; r < n; ++r)
             bulk_s2g(reinterpret_cast<unsigned char*>(const_cast<float*>(stage.p[r])) + k0 * C::ES,
-                     raw + rs * C::RAW_BYTES + r * C::RAW_PITCH, bytes);
+                     raw + rs * raw_bytes + r * C::RAW_PITCH, bytes);
           bulk_commit();
         }
         for (int64_t k = k0 + cb; k < k0 + cnt; ++k) {   // ragged tail: < 16 bytes per row
@@ -260,8 +281,8 @@ __global__ void __launch_bounds__(Cfg<NP, BF>::THREADS, 1)
         const int64_t i = j * C::RAW_SUB + sub;
         if (i >= T) break;
         const int s = static_cast<int>(i % C::OP_STAGES);
-        const unsigned char* rt = raw_me + rs * C::RAW_BYTES + sub * C::KT * C::ES;
-        const unsigned char* rtc = raw_c + rs * C::RAW_BYTES + sub * C::KT * C::ES;
+        const unsigned char* rt = raw_me + rs * raw_bytes + sub * C::KT * C::ES;
+        const unsigned char* rtc = raw_c + rs * raw_bytes + sub * C::KT * C::ES;
         // the tile holding coordinate d-1 may end in a (< 4-coordinate) chunk the
         // bulk copy skipped; only that tile pays for 64-bit bounds checks
         const bool last_tile = (t0 + i + 1) * C::KT > d;
@@ -464,7 +485,16 @@ cudaError_t launch_np(const RowPtrs& rp, int n, int64_t d, double* partials, int
   auto kern = staged ? gram_tc_kernel<NP, true, BF> : gram_tc_kernel<NP, false, BF>;
   cudaError_t e = cached_occupancy(kern, C::THREADS, C::SMEM_BYTES, &occ);
   if (e != cudaSuccess) return e;
-  kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(rp, n, d, tiles, partials, l2_evict_first_enabled(), stage);
+  // raw ring: round_up(n, 8) rows per stage, as many stages as fit.  The
+  // converters read all NP rows of a stage (rows >= n are never stored), so the
+  // region keeps NP - round_up(n, 8) rows of slack after the last stage.
+  const int n8 = (n + 7) / 8 * 8;
+  const int raw_bytes = n8 * C::RAW_PITCH;
+  int raw_stages = (C::RAW_REGION - (NP - n8) * C::RAW_PITCH) / raw_bytes;
+  if (raw_stages > C::RAW_STAGES_MAX) raw_stages = C::RAW_STAGES_MAX;
+  if (C::RAW_STAGES_FIXED > 0 && raw_stages > C::RAW_STAGES_FIXED) raw_stages = C::RAW_STAGES_FIXED;
+  kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(rp, n, d, tiles, partials, l2_evict_first_enabled(), stage,
+                                                     raw_stages, raw_bytes);
   *n_parts = grid;
   return cudaGetLastError();
 }
