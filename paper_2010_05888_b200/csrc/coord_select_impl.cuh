@@ -652,7 +652,11 @@ inline cudaError_t launch_mode(const CoordLaunch& L, cudaStream_t stream) {
     return launch_mode_w<MODE, N, consumer_warps<MODE, N>(), T>(L, stream);
   } else {
     if (L.R <= 32) return launch_mode_w<MODE, 0, 15, T>(L, stream);
-    return launch_mode_w<MODE, 0, 7, T>(L, stream);
+    // above 32 rows: fp32 keeps the measured 7 consumer warps (3 stages);
+    // bf16 rows (two coordinates per thread, F2F-heavy sums) take 12 (2 stages
+    // of <= 97 KB): C5 sweep, bf16 Average at n = 35: 0.52 ms with 7
+    if constexpr (std::is_same<T, float>::value) return launch_mode_w<MODE, 0, 7, T>(L, stream);
+    else return launch_mode_w<MODE, 0, 12, T>(L, stream);
   }
 }
 
