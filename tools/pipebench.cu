@@ -68,6 +68,8 @@ __global__ void bench(float* out, float seed, long long* clk) {
       if (KIND == 12) { double d; asm volatile("cvt.f64.f32 %0, %1;" : "=d"(d) : "f"(f[k])); f[(k + 1) & 7] += (float)0 * (float)d; iv[k] ^= __double2loint(d); }  // F2F.F64
       if (KIND == 13) { uint32_t r; asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(f[k]), "f"(f[(k + 1) & 7])); h[k] ^= r; f[k] = fmn(f[k], f[(k + 2) & 7]); }  // F2FP + FMNMX
       if (KIND == 14) { double d; asm volatile("cvt.f64.f32 %0, %1;" : "=d"(d) : "f"(f[k])); iv[k] ^= __double2loint(d); uint32_t r; asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(f[(k + 1) & 7]), "f"(f[(k + 2) & 7])); h[k] ^= r; }  // F2F + F2FP
+      if (KIND == 16) { double a = __hiloint2double(iv[k], iv[(k + 1) & 7]); double b = __hiloint2double(iv[(k + 2) & 7], iv[k]); double r; asm volatile("min.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b)); iv[k] = __double2loint(r); }  // DMNMX
+      if (KIND == 17) { double a = __hiloint2double(iv[k], iv[(k + 1) & 7]); double b = __hiloint2double(iv[(k + 2) & 7], iv[k]); double r; asm volatile("min.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b)); iv[k] = __double2loint(r); f[k] = fmn(f[k], f[(k + 1) & 7]); }  // DMNMX + FMNMX
       if (KIND == 15) { double d = __int_as_float(iv[k]) * 1.0; asm volatile("fma.rn.f64 %0, %1, %2, %3;" : "=d"(d) : "d"(d), "d"(d), "d"(d)); iv[k] = __double2loint(d); }  // DFMA (+F2F)
     }
   }
@@ -87,9 +89,9 @@ int main() {
   cudaMalloc(&clk, blocks * 8);
   const char* names[] = {"FMNMX", "IMNMX", "HMNMX2.BF16", "FMNMX+IMNMX", "FMNMX+HMNMX2", "FMNMX.NAN",
                          "VIMNMX s16x2", "FMNMX+VIMNMX", "FMNMX3", "FADD", "FMNMX+IMAD", "F2FP.PACK",
-                         "F2F.F64.F32", "F2FP+FMNMX", "F2F+F2FP", "DFMA(+F2F)"};
-  int ops[] = {1, 1, 1, 2, 2, 1, 1, 2, 1, 1, 2, 1, 1, 2, 2, 2};
-  for (int kind = 0; kind < 16; ++kind) {
+                         "F2F.F64.F32", "F2FP+FMNMX", "F2F+F2FP", "DFMA(+F2F)", "DMNMX", "DMNMX+FMNMX"};
+  int ops[] = {1, 1, 1, 2, 2, 1, 1, 2, 1, 1, 2, 1, 1, 2, 2, 2, 1, 2};
+  for (int kind = 0; kind < 18; ++kind) {
     for (int rep = 0; rep < 2; ++rep) {
       switch (kind) {
         case 0: bench<0><<<blocks, threads>>>(out, 1.f, clk); break;
@@ -108,6 +110,8 @@ int main() {
         case 13: bench<13><<<blocks, threads>>>(out, 1.f, clk); break;
         case 14: bench<14><<<blocks, threads>>>(out, 1.f, clk); break;
         case 15: bench<15><<<blocks, threads>>>(out, 1.f, clk); break;
+        case 16: bench<16><<<blocks, threads>>>(out, 1.f, clk); break;
+        case 17: bench<17><<<blocks, threads>>>(out, 1.f, clk); break;
       }
     }
     cudaDeviceSynchronize();
