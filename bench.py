@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--workload", default="C3", help="C1..C4 or sweep:<n>")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "peer", "nccl"],
+                    help="N>1 Krum-family Gram exchange: peer-memory kernels (auto/peer) or NCCL all-reduce")
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"],
                     help="element type of the gradients (bf16: SURVEY §8f-4, widened exactly, DESIGN.md R16)")
     ap.add_argument("--no-variants", action="store_true",
@@ -85,27 +87,36 @@ def rule_bytes(rule, n, f, d, es=4):
 
 
 class Clocks:
-    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line):
+    ONE process per node (local rank 0) querying every GPU every 200 ms, started
+    before the ranks' pre-timing barrier (profiles/r2_multigpu.md: starting a
+    sampler between the barrier and t0 skewed the ranks by nvidia-smi's start-up
+    time, which the earliest rank then timed at its first cross-rank sync)."""
 
-    def __init__(self, index):
+    def __init__(self, index, active=True):
         self.index = index
+        self.active = active
         self.proc = None
         self.path = None
 
     def __enter__(self):
+        if not self.active:
+            return self
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+            if os.environ.get("GAR_BENCH_NO_SMI"):         # diagnostics only: no sampler
+                raise RuntimeError("sampler disabled")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
         # the sampler must be running before the timed region starts: wait for
-        # its first line (nvidia-smi can take a second to start on a cold box)
+        # its first lines (nvidia-smi can take a second to start on a cold box)
         t_end = time.time() + 5.0
         while self.proc is not None and time.time() < t_end:
             try:
@@ -121,22 +132,28 @@ class Clocks:
         try:
             with open(self.path) as fh:
                 return sum(1 for _ in fh)
-        except OSError:
+        except (OSError, TypeError):
             return 0
 
     def __exit__(self, *a):
-        # keep sampling until at least two samples cover the timed region
+        # keep sampling until one more round of samples covers the timed region
         t_end = time.time() + 2.0
-        while self.proc is not None and self._count() < self._lines0 + 2 and time.time() < t_end:
+        while self.proc is not None and self._count() <= self._lines0 and time.time() < t_end:
             time.sleep(0.05)
         if self.proc:
             self.proc.terminate()
             self.proc.wait()
 
-    def summary(self):
+    def summary(self, gpus=None):
+        """Median SM clock under load, max clock and throttle reasons over the
+        job's GPUs (indices `gpus`, default all sampled)."""
+        if not self.active:
+            return None
         try:
             rows = [l.split(",") for l in open(self.path).read().strip().splitlines()]
             rows = [[c.strip() for c in r] for r in rows if len(r) >= 9]
+            if gpus is not None:
+                rows = [r for r in rows if int(r[0]) in gpus]
             sm = [float(r[1]) for r in rows]
             mx = max(float(r[2]) for r in rows)
             reasons = set()
@@ -206,7 +223,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     from paper_2010_05888_b200.dist import ShardedAggregator, shard_len
-    aggs = {r: ShardedAggregator(r, n, f, d, output=args.output) for r in RULES}
+    aggs = {r: ShardedAggregator(r, n, f, d, output=args.output, exchange=args.exchange) for r in RULES}
     outs = {r: torch.empty(dl, dtype=torch.float32, device=dev) for r in RULES}
     full = {r: torch.empty(shard_len(d, world) * world, dtype=torch.float32, device=dev) for r in RULES} \
         if world > 1 else {r: None for r in RULES}
@@ -244,9 +261,12 @@ def run_ours(args):
         for _ in range(warmup):
             step(Xin, None)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        with Clocks(local) as clk:
+        # the sampler starts (and delivers its first sample) BEFORE the ranks'
+        # barrier: a rank that entered the timed region while another still
+        # waited for nvidia-smi would time that wait at its first cross-rank sync
+        with Clocks(local, active=(local == 0)) as clk:
+            if world > 1:
+                dist.barrier()
             torch.cuda.synchronize()
             t0 = ev()
             for _ in range(steps):
@@ -255,7 +275,10 @@ def run_ours(args):
             torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        return t0.elapsed_time(t1), segs, clk.summary()
+        # the job's GPUs: cuda:0..N-1 are nvidia-smi indices 0..N-1 unless remapped
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        gpus = set(range(world)) if not vis else {int(v) for v in vis.split(",")[:world] if v.strip().isdigit()}
+        return t0.elapsed_time(t1), segs, clk.summary(gpus or None)
 
     def rule_times(segs):
         cls_ms, rule_ms = {}, {r: 0.0 for r in RULES}
@@ -267,6 +290,11 @@ def run_ours(args):
 
     ms, segs, clocks = measure(X, args.steps, args.warmup)
     cls_ms, rule_ms = rule_times(segs)
+    if os.environ.get("GAR_BENCH_PER_RANK"):    # diagnostics: this rank's own times (stderr)
+        print(json.dumps({"rank": rank, "ms_per_step": round(ms / args.steps, 4),
+                          "per_rule": {r: round(t / args.steps, 4) for r, t in rule_ms.items()},
+                          "stages": {c: round(t / args.steps, 4) for c, t in cls_ms.items()}}),
+              file=sys.stderr, flush=True)
     if world > 1:
         t = torch.tensor([ms] + [rule_ms[r] for r in RULES], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
