@@ -24,6 +24,13 @@ cudaError_t launch_gram_partials(const float* const* rows, int n, int64_t d, dou
                                  int num_sms, int* n_parts, cudaStream_t stream,
                                  float* const* stage_rows = nullptr, int dtype = 0 /* ElemType */);
 
+// The same contract on the CUDA cores (fp32 FFMA, all n(n+1)/2 products per
+// lane, fp64 across stages; gram_cc.cu) for n <= kGramCcMaxN; launch_gram_partials
+// uses it there.
+constexpr int kGramCcMaxN = 12;
+cudaError_t launch_gram_cc(const float* const* rows, int n, int64_t d, double* partials, int num_sms,
+                           int* n_parts, cudaStream_t stream, int dtype);
+
 // G = sum_p partials[p] in fixed order p = 0..n_parts-1 (deterministic).
 cudaError_t launch_gram_reduce(const double* partials, int n_parts, int n, double* G,
                                cudaStream_t stream);
