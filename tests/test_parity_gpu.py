@@ -259,7 +259,7 @@ def test_mean_around_median_parity(gar, n, f):
     assert_same_bits(out.cpu().numpy(), oracle.mean_around_median(x, f), "mean around median")
 
 
-GRAM_CC_MAX_N = 12   # csrc/gram.h kGramCcMaxN: the CUDA-core Gram below it, the tensor cores above
+GRAM_CC_MAX_N = 12   # csrc/gram.h kGramCcMaxN: the CUDA-core Gram up to it, the tensor cores above
 
 
 @pytest.mark.parametrize("n,d", [(7, 100_003), (12, 100_003), (31, 300_001), (64, 20_003)])
