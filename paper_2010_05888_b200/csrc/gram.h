@@ -27,7 +27,7 @@ cudaError_t launch_gram_partials(const float* const* rows, int n, int64_t d, dou
 // The same contract on the CUDA cores (fp32 FFMA, all n(n+1)/2 products per
 // lane, fp64 across stages; gram_cc.cu) for n <= kGramCcMaxN; launch_gram_partials
 // uses it there.
-constexpr int kGramCcMaxN = 12;
+constexpr int kGramCcMaxN = 15;
 cudaError_t launch_gram_cc(const float* const* rows, int n, int64_t d, double* partials, int num_sms,
                            int* n_parts, cudaStream_t stream, int dtype);
 

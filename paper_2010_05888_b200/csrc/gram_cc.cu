@@ -11,7 +11,7 @@
 // multiplied in fp32 FFMA (one rounding per product-add, more accurate than
 // the tf32 split).
 //
-// Layout (n <= 12, every loop unrolled for the exact n): each element is read
+// Layout (n <= 15, every loop unrolled for the exact n): each element is read
 // from the TMA ring once; a lane keeps all n(n+1)/2 products-sums of the
 // coordinates it visits (consumer warp w owns part w of every raw stage, lane
 // l its coordinates l, l+32, ...), in fp32 over FLUSH_ST stages (32 coordinates
@@ -45,10 +45,12 @@ struct CfgCC {
   static constexpr int BULK_ALIGN = 16 / ES;
   static constexpr int NPAIR = N * (N + 1) / 2;   // upper triangle incl. the diagonal
   static constexpr int NACC = (NPAIR + 31) / 32 * 32;   // accumulators per lane (butterfly needs 32 | NACC)
-  static constexpr int CONS_WARPS = 12;           // coordinate parts of a stage, one per warp
-  static constexpr int PROD_WARPS = 3;
+  // registers are allocated per 4-warp group: 15 warps leave 128 per thread
+  // (<= 96 accumulators, n <= 12); 8 warps leave 255 (<= 128, n <= 15)
+  static constexpr int CONS_WARPS = N <= 12 ? 12 : 7;   // coordinate parts of a stage, one per warp
+  static constexpr int PROD_WARPS = N <= 12 ? 3 : 1;
   static constexpr int THREADS = (CONS_WARPS + PROD_WARPS) * 32;
-  static constexpr int RAW_KT = 1536;             // coordinates per raw stage (6 KB per fp32 row)
+  static constexpr int RAW_KT = CONS_WARPS * 128;       // coordinates per raw stage
   static constexpr int PART = RAW_KT / CONS_WARPS;      // 128 coordinates per warp and stage
   static constexpr int PER_LANE = PART / 32;            // 4
   static constexpr int FLUSH_ST = 8;              // stages summed in fp32 per lane (32 coordinates)
@@ -59,7 +61,7 @@ struct CfgCC {
   static constexpr int SMEM_BYTES = 227 * 1024;
   static constexpr int BAR_BYTES = (PROD_WARPS + 1) * RAW_STAGES_MAX * 8 + 16;
   static constexpr int RAW_REGION = SMEM_BYTES - 128 - SCRATCH - WSUM_BYTES - BAR_BYTES;
-  static_assert(N >= 1 && N <= 12, "one accumulator set of <= 96 per lane");
+  static_assert(N >= 1 && NACC <= 128, "one accumulator set of <= 128 per lane");
   static_assert(RAW_KT % (32 * CONS_WARPS) == 0, "work split");
   static_assert(RAW_REGION >= 2 * NP * RAW_PITCH, "two raw stages");
 };
