@@ -30,6 +30,13 @@ cudaError_t launch_gram_partials(const float* const* rows, int n, int64_t d, dou
 constexpr int kGramCcMaxN = 15;
 cudaError_t launch_gram_cc(const float* const* rows, int n, int64_t d, double* partials, int num_sms,
                            int* n_parts, cudaStream_t stream, int dtype);
+// ... and for kGramCcMaxN < n <= kGramCckLimit with the pair triangle cut into
+// two chunks over warps (gram_cck.cu); launch_gram_partials uses it up to
+// kGramCckMaxN.
+constexpr int kGramCckLimit = 22;
+constexpr int kGramCckMaxN = 22;
+cudaError_t launch_gram_cck(const float* const* rows, int n, int64_t d, double* partials, int num_sms,
+                            int* n_parts, cudaStream_t stream, int dtype);
 
 // G = sum_p partials[p] in fixed order p = 0..n_parts-1 (deterministic).
 cudaError_t launch_gram_reduce(const double* partials, int n_parts, int n, double* G,

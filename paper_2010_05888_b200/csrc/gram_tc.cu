@@ -515,10 +515,10 @@ cudaError_t launch_gram_t(const float* const* rows, int n, int64_t d, double* pa
 
 }  // namespace
 
-// Kernel choice: CUDA-core FFMA Gram (gram_cc.cu) for n <= kGramCcMaxN rows,
-// the tensor-core kernel above it (and for the fused ingress staging, which
-// only the tensor-core kernel implements).  GAR_GRAM_CC=0 forces the tensor
-// cores (A/B measurements).
+// Kernel choice: CUDA-core FFMA Gram (gram_cc.cu n <= kGramCcMaxN, gram_cck.cu
+// n <= kGramCckMaxN), the tensor-core kernel above (and for the fused ingress
+// staging, which only the tensor-core kernel implements).  GAR_GRAM_CC=0
+// forces the tensor cores, =1 the CUDA cores up to kGramCckLimit (A/B).
 static int gram_cc_forced() {
   static const int v = [] {
     const char* e = getenv("GAR_GRAM_CC");
@@ -530,8 +530,11 @@ static int gram_cc_forced() {
 cudaError_t launch_gram_partials(const float* const* rows, int n, int64_t d, double* partials, int num_sms,
                                  int* n_parts, cudaStream_t stream, float* const* stage_rows, int dtype) {
   const int forced = gram_cc_forced();
-  const bool cc = !stage_rows && n <= kGramCcMaxN && forced != 0;
-  if (cc) return launch_gram_cc(rows, n, d, partials, num_sms, n_parts, stream, dtype);
+  if (!stage_rows && forced != 0) {
+    if (n <= kGramCcMaxN) return launch_gram_cc(rows, n, d, partials, num_sms, n_parts, stream, dtype);
+    if (n <= (forced == 1 ? kGramCckLimit : kGramCckMaxN))
+      return launch_gram_cck(rows, n, d, partials, num_sms, n_parts, stream, dtype);
+  }
   if (dtype == kBF16) return launch_gram_t<true>(rows, n, d, partials, num_sms, n_parts, stream, stage_rows);
   if (dtype != kF32) return cudaErrorInvalidValue;
   return launch_gram_t<false>(rows, n, d, partials, num_sms, n_parts, stream, stage_rows);

@@ -259,15 +259,15 @@ def test_mean_around_median_parity(gar, n, f):
     assert_same_bits(out.cpu().numpy(), oracle.mean_around_median(x, f), "mean around median")
 
 
-GRAM_CC_MAX_N = 15   # csrc/gram.h kGramCcMaxN: the CUDA-core Gram up to it, the tensor cores above
+GRAM_CC_MAX_N = 22   # csrc/gram.h kGramCckMaxN: the CUDA-core Gram up to it, the tensor cores above
 
 
-@pytest.mark.parametrize("n,d", [(7, 100_003), (15, 100_003), (31, 300_001), (64, 20_003)])
+@pytest.mark.parametrize("n,d", [(7, 100_003), (15, 100_003), (19, 100_003), (31, 300_001), (64, 20_003)])
 def test_gram_exchange_single_rank_and_staging(gar, n, d):
     """gar_gram_exchange with world = 1 (slots and flags in this GPU's memory):
     the flag handshake completes, G equals gar_gram_partial's bit for bit, and
     the staging copy (the fused ingress of the d-sharded path) equals the rows.
-    The staging copy exists only in the tensor-core Gram, so for n <= 15 a
+    The staging copy exists only in the tensor-core Gram, so for n <= 22 a
     staged exchange runs the other kernel than gar_gram_partial: equal there
     in D within the 1e-5 bar."""
     x = synth.make_gradients(n, (n - 3) // 4 if n >= 3 else 0, d, seed=5 + n, ld=d).numpy()

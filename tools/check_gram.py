@@ -17,7 +17,7 @@ def run(x):
     return D.cpu().numpy()
 
 for (n, f, d, kind) in [(3, 0, 128, "clean"), (5, 1, 1000, "byzantine"), (7, 1, 300001, "byzantine"),
-                        (8, 1, 4093, "clean"), (10, 1, 77777, "byzantine"), (11, 2, 79510, "byzantine"), (12, 2, 250001, "clean"), (13, 2, 99999, "byzantine"), (15, 3, 333333, "clean"), (17, 3, 5000, "byzantine"),
+                        (8, 1, 4093, "clean"), (10, 1, 77777, "byzantine"), (11, 2, 79510, "byzantine"), (12, 2, 250001, "clean"), (13, 2, 99999, "byzantine"), (15, 3, 333333, "clean"), (16, 3, 77777, "clean"), (17, 3, 5000, "byzantine"), (22, 4, 222222, "byzantine"),
                         (19, 4, 1756426, "byzantine"), (23, 5, 123457, "clean"),
                         (31, 7, 300001, "byzantine"), (32, 7, 4096, "clean"), (33, 7, 50000, "byzantine"),
                         (64, 15, 100003, "byzantine")]:

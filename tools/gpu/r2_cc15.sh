@@ -2,7 +2,7 @@
 cd $GRAFT_REPO_ROOT
 o=gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > $o/build.log 2>&1 || { tail -20 $o/build.log; exit 1; }
-NS="7 11 12 13 14 15 16"
+NS="${NS:-7 11 12 13 14 15 16}"
 timeout 300 python tools/gram_time.py $NS 2>&1 | tail -1
 GAR_GRAM_CC=0 timeout 300 python tools/gram_time.py $NS 2>&1 | tail -1
 timeout 600 python tools/check_gram.py 2>&1 | head -12

@@ -4,7 +4,7 @@ o=gpurun_out
 N=${1:-31}
 python -c "import __graft_entry__ as g; g.build()" > $o/build.log 2>&1 || { tail -20 $o/build.log; exit 1; }
 timeout 300 python tools/gram_time.py $N 2>&1 | tail -1
-GAR_GRAM_CC=1 timeout 600 ncu --set full --import-source on --clock-control none -k regex:gram_ccb -s 2 -c 1 -o /tmp/ccb -f python tools/gram_one.py $N > $o/ccb_ncu.log 2>&1; echo "ncu rc=$?"
+GAR_GRAM_CC=1 timeout 600 ncu --set full --import-source on --clock-control none -k regex:${KREGEX:-gram_ccb} -s 2 -c 1 -o /tmp/ccb -f python tools/gram_one.py $N > $o/ccb_ncu.log 2>&1; echo "ncu rc=$?"
 ncu -i /tmp/ccb.ncu-rep --page source --csv --print-source cuda,sass > /tmp/ccb_src.csv 2>&1
 python tools/ncu_lines.py /tmp/ccb_src.csv 30 > $o/ccb_lines.txt 2>&1
 ncu -i /tmp/ccb.ncu-rep --page details --csv > $o/ccb_details.csv 2>&1
