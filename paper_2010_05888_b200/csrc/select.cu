@@ -1,177 +1,21 @@
 // select.cu — from the summed Gram matrix to the Krum / Multi-Krum / Bulyan
-// selection (rows a5 epilogue, a6, a7 of DESIGN.md §1).  One CTA: the n x n
-// problem (n <= 64) is tiny; everything lives in shared memory.
-//
-//   D_ij = G_ii + G_jj - 2 G_ij   (fp64, evaluated once per unordered pair so D
-//          is bitwise symmetric; < 0 -> 0; non-finite or > FLT_MAX -> +inf, R4)
-//   row i sorted ascending by (D_ij, j) via rank counting (n^3 independent
-//   compares spread over 256 threads)
-//   Krum score s_i = sum of the k smallest D_ij, j in pool, j != i, in ascending
-//   order (fp64), k = n-f-2 (Multi-Krum) or max(|R|-f-2, 0) (Bulyan round, R7)
-//   Multi-Krum: the m smallest (s_i, i);  Bulyan: theta = n-2f rounds of
-//   argmin (s_i, i) with removal, on the same cached D.
-#include <cfloat>
-#include <cmath>
-
-#include "common.cuh"
-#include "gram.h"
+// selection (rows a5 epilogue, a6, a7 of DESIGN.md §1) as its own launch: one
+// CTA of 256 threads runs sel::select_block (select_block.cuh; the n x n
+// problem, n <= 64, lives in shared memory).
+#include "select_block.cuh"
 
 namespace gar {
 
 namespace {
 
 constexpr int kSelThreads = 256;
-constexpr size_t kDmBytes = sizeof(double) * GAR_MAX_N * (GAR_MAX_N + 1);
-constexpr size_t kSdBytes = sizeof(double) * GAR_MAX_N * GAR_MAX_N;
-constexpr size_t kSelSmem = kDmBytes + kSdBytes + GAR_MAX_N * GAR_MAX_N;
-
-__device__ __forceinline__ bool key_lt(double a, int ia, double b, int ib) {
-  return a < b || (a == b && ia < ib);
-}
 
 __global__ void __launch_bounds__(kSelThreads) select_kernel(const double* __restrict__ G, int n, int f, int m,
                                                              int rule, int32_t* __restrict__ idx_out,
                                                              double* __restrict__ D_out) {
   extern __shared__ __align__(16) unsigned char sel_smem[];
-  auto Dm = reinterpret_cast<double (*)[GAR_MAX_N + 1]>(sel_smem);                  // [64][65]
-  auto sd = reinterpret_cast<double (*)[GAR_MAX_N]>(sel_smem + kDmBytes);           // row i ascending, j != i
-  auto sj = reinterpret_cast<unsigned char (*)[GAR_MAX_N]>(sel_smem + kDmBytes + kSdBytes);
-  __shared__ double score[GAR_MAX_N];
-  __shared__ unsigned long long pool;
-
-  const int tid = threadIdx.x;
-  for (int e = tid; e < n * n; e += kSelThreads) {
-    const int i = e / n, j = e % n;
-    double v = 0.0;
-    if (i != j) {
-      const int a = min(i, j), b = max(i, j);
-      v = G[a * n + a] + G[b * n + b] - 2.0 * G[a * n + b];
-      if (!(v >= 0.0)) v = (v < 0.0) ? 0.0 : INFINITY;   // NaN -> +inf, negative -> 0
-      if (v > static_cast<double>(FLT_MAX)) v = INFINITY;
-    }
-    Dm[i][j] = v;
-    if (D_out) D_out[e] = v;
-  }
-  __syncthreads();
-  if (rule == kSelDistancesOnly) return;
-
-  // rank of (D_ij, j) within row i (j != i) -> position in the sorted row
-  for (int e = tid; e < n * n; e += kSelThreads) {
-    const int i = e / n, j = e % n;
-    if (i == j) continue;
-    const double v = Dm[i][j];
-    int r = 0;
-    for (int k = 0; k < n; ++k)
-      if (k != i && key_lt(Dm[i][k], k, v, j)) ++r;
-    sd[i][r] = v;
-    sj[i][r] = static_cast<unsigned char>(j);
-  }
-  if (tid == 0) pool = (n == 64) ? ~0ull : ((1ull << n) - 1ull);
-  __syncthreads();
-
-  if (rule == kSelMultiKrum) {
-    const int k = n - f - 2;
-    if (tid < n) {
-      double s = 0.0;
-      for (int r = 0; r < k; ++r) s += sd[tid][r];
-      score[tid] = s;
-    }
-    __syncthreads();
-    if (tid < n) {
-      int r = 0;
-      for (int j = 0; j < n; ++j)
-        if (key_lt(score[j], j, score[tid], tid)) ++r;
-      if (r < m) idx_out[r] = tid;
-    }
-    return;
-  }
-
-  const int theta = n - 2 * f;
-  if (n <= 32) {
-    // Bulyan, n <= 32: one warp, lane i holds row i's sorted distances in
-    // registers; each round sums the k smallest pool members in ascending
-    // order (the same fp64 additions as below) and a shuffle argmin picks the
-    // lowest (score, index).  No block barriers.
-    if (tid < 32) {
-      const int i = tid;
-      double row[31];
-      int rj[31];
-#pragma unroll
-      for (int e = 0; e < 31; ++e) {
-        const bool ok = i < n && e < n - 1;
-        row[e] = ok ? sd[i][e] : 0.0;
-        rj[e] = ok ? sj[i][e] : 63;
-      }
-      unsigned long long P = (1ull << n) - 1ull;
-      for (int t = 0; t < theta; ++t) {
-        const int k = max(__popcll(P) - f - 2, 0);
-        double sc = 0.0;
-        int taken = 0;
-#pragma unroll
-        for (int e = 0; e < 31; ++e) {
-          const bool take = ((P >> rj[e]) & 1ull) && taken < k;
-          if (take) sc += row[e];
-          taken += take ? 1 : 0;
-        }
-        double best = (i < n && ((P >> i) & 1ull)) ? sc : INFINITY;
-        int bi = (i < n && ((P >> i) & 1ull)) ? i : (1 << 30);
-        for (int off = 16; off > 0; off >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-          if (key_lt(ob, oi, best, bi)) {
-            best = ob;
-            bi = oi;
-          }
-        }
-        if (i == 0) idx_out[t] = bi;
-        P &= ~(1ull << bi);
-      }
-    }
-    return;
-  }
-
-  // Bulyan: theta rounds of Krum with removal (R7)
-  for (int t = 0; t < theta; ++t) {
-    const unsigned long long P = pool;
-    const int psize = __popcll(P);
-    const int k = max(psize - f - 2, 0);
-    if (tid < n && ((P >> tid) & 1ull)) {
-      double s = 0.0;
-      int taken = 0;
-      for (int r = 0; r < n - 1 && taken < k; ++r) {
-        if ((P >> sj[tid][r]) & 1ull) {
-          s += sd[tid][r];
-          ++taken;
-        }
-      }
-      score[tid] = s;
-    }
-    __syncthreads();
-    if (tid < 32) {
-      // argmin over (score, index) in the pool: lanes cover i and i + 32
-      double best = INFINITY;
-      int bi = 1 << 30;
-      for (int i = tid; i < n; i += 32) {
-        if (((P >> i) & 1ull) && key_lt(score[i], i, best, bi)) {
-          best = score[i];
-          bi = i;
-        }
-      }
-      for (int off = 16; off > 0; off >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (key_lt(ob, oi, best, bi)) {
-          best = ob;
-          bi = oi;
-        }
-      }
-      if (tid == 0) {
-        idx_out[t] = bi;
-        pool = P & ~(1ull << bi);
-      }
-    }
-    __syncthreads();
-  }
+  sel::select_block(G, n, f, m, rule, idx_out, D_out, *reinterpret_cast<sel::SelSmem*>(sel_smem), threadIdx.x,
+                    kSelThreads, 1);
 }
 
 }  // namespace
@@ -179,9 +23,9 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const double* __res
 cudaError_t launch_select(const double* G, int n, int f, int m, int rule, int32_t* idx_out, double* D_out,
                           cudaStream_t stream) {
   int occ = 0;
-  cudaError_t e = cached_occupancy(select_kernel, kSelThreads, kSelSmem, &occ);
+  cudaError_t e = cached_occupancy(select_kernel, kSelThreads, sizeof(sel::SelSmem), &occ);
   if (e != cudaSuccess) return e;
-  select_kernel<<<1, kSelThreads, kSelSmem, stream>>>(G, n, f, m, rule, idx_out, D_out);
+  select_kernel<<<1, kSelThreads, sizeof(sel::SelSmem), stream>>>(G, n, f, m, rule, idx_out, D_out);
   return cudaGetLastError();
 }
 
