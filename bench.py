@@ -184,7 +184,11 @@ def traffic_from_profiles(kernel, workload, world):
     try:
         with open(path) as fh:
             t = json.load(fh)
-        return t.get("per_kernel", {}).get(kernel.split("<")[0])
+        base = kernel.split("<")[0]
+        for k, v in t.get("per_kernel", {}).items():   # ncu names carry a namespace prefix
+            if k.split("::")[-1].split("<")[0] == base:
+                return v
+        return None
     except Exception:
         return None
 

@@ -12,14 +12,18 @@
 // fp32 accumulators are drained every FLUSH tiles into fp64 registers.
 //
 // Warp roles (one persistent CTA per SM):
-//   6-8 warps   loaders (warp = 16-coordinate slice of the tile, lane = 8 row
-//               groups x 4 chunks): LDG.128 streaming loads with a P-deep
-//               register prefetch ring, centring by warp shuffle, hi/lo split,
-//               STS into the
-//               SWIZZLE_128B K-major operand layout, fence.proxy.async, arrive;
+//   3 warps     TMA producers: one 1D bulk copy per row per raw stage into the
+//               raw ring (rows q mod 3 per warp, one mbarrier each);
+//   4-8 warps   converters (warp = 16-coordinate slice of the tile, lane = 8 row
+//               groups x 4 chunks): LDS.128 from the raw ring, centring, hi/lo
+//               split, STS into the SWIZZLE_128B K-major operand layout,
+//               fence.proxy.async, arrive (loads straight from global memory
+//               were measured 2x slower: profiles/r1_gram_experiments.md §4);
 //   4 or 8 warps epilogue: tcgen05.ld of the accumulator lanes -> fp64 sums
 //               (8 when NP = 64: each thread owns half of a 64-column row);
 //   last warp   TMEM allocator + single-thread tcgen05.mma issuer.
+// n <= kGramCckMaxN goes to the CUDA-core kernels instead (gram_cc.cu,
+// gram_cck.cu; launch_gram_partials below).
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>

@@ -75,3 +75,17 @@ def test_our_arm_line_bf16():
     e = j["e2e"]
     assert n * d * 2 <= e["h2d_bytes_per_step"] < n * (d + 64) * 2
     assert j["roofline"]["frac"] > 0
+
+
+def test_roofline_traffic_from_committed_capture():
+    """roofline.traffic of the default C3 line = dram read + write per launch of
+    the dominant kernel from the committed ncu --set full capture
+    (profiles/traffic.json); it must be within 1 % of the kernel's algorithmic
+    bytes (n*d*4 read), i.e. no wasted re-reads.  Other workloads: null."""
+    import bench
+    import synth
+    cfg = synth.CONFIGS["C3"]
+    t = bench.traffic_from_profiles("gram_tc_kernel<32>", "C3", 1)
+    assert t is not None and abs(t / (cfg.n * cfg.d * 4) - 1) < 0.01
+    assert bench.traffic_from_profiles("gram_tc_kernel<32>", "C1", 1) is None
+    assert bench.traffic_from_profiles("gram_tc_kernel<32>", "C3", 2) is None
