@@ -51,10 +51,12 @@ def parse():
                     help="element type of the gradients (bf16: SURVEY §8f-4, widened exactly, DESIGN.md R16)")
     ap.add_argument("--no-variants", action="store_true",
                     help="skip the bf16 variant measured after the fp32 line's timed region (N=1)")
-    ap.add_argument("--output", default="fused",
+    ap.add_argument("--output", default="sharded",
                     choices=["replicated", "replicated-async", "sharded", "fused", "fused-mc"],
-                    help="N>1: all-gather the aggregate to every rank with NCCL (north_star), write it into every "
-                         "rank's buffer from the producing kernel over NVLink (fused), or keep it d-sharded")
+                    help="N>1: keep the aggregate d-sharded (the primary number, SURVEY.md §8e: a ZeRO-style "
+                         "consumer updates its own parameter shard), all-gather it to every rank with NCCL, or "
+                         "write it into every rank's buffer from the producing kernel over NVLink (fused); with "
+                         "sharded, the fused replicated output is measured after the timed region as a variant")
     return ap.parse_args()
 
 
@@ -241,13 +243,14 @@ def run_ours(args):
         e.record(stream)
         return e
 
-    def step(Xin, segs):
+    def step(Xin, segs, A=None):
         # fused output: one cross-GPU barrier per step (the last rule's), which
         # makes all six replicated outputs readable (dist.ShardedAggregator.sync)
+        A = A or aggs
         for r in RULES:
             last_rule = r == RULES[-1]
             if segs is None:
-                aggs[r].aggregate(Xin, out_local=outs[r], out_full=full[r], barrier=last_rule)
+                A[r].aggregate(Xin, out_local=outs[r], out_full=full[r], barrier=last_rule)
                 continue
             last = [ev()]
 
@@ -255,15 +258,15 @@ def run_ours(args):
                 e = ev()
                 segs.append((label, r, last[0], e))
                 last[0] = e
-            aggs[r].aggregate(Xin, out_local=outs[r], out_full=full[r], mark=mark, barrier=last_rule)
+            A[r].aggregate(Xin, out_local=outs[r], out_full=full[r], mark=mark, barrier=last_rule)
         for r in RULES:              # output="replicated-async": the step ends when every gather has
-            aggs[r].wait()           # landed (they overlap the following rules' kernels)
+            A[r].wait()              # landed (they overlap the following rules' kernels)
 
-    def measure(Xin, steps, warmup, clocks=True):
+    def measure(Xin, steps, warmup, clocks=True, A=None):
         """(ms over `steps` steps, segments, clock summary), max over ranks."""
         segs = []
         for _ in range(warmup):
-            step(Xin, None)
+            step(Xin, None, A)
         torch.cuda.synchronize()
         # the sampler starts (and delivers its first sample) BEFORE the ranks'
         # barrier: a rank that entered the timed region while another still
@@ -274,7 +277,7 @@ def run_ours(args):
             torch.cuda.synchronize()
             t0 = ev()
             for _ in range(steps):
-                step(Xin, segs)
+                step(Xin, segs, A)
             t1 = ev()
             torch.cuda.synchronize()
         if world > 1:
@@ -389,6 +392,19 @@ def run_ours(args):
         X16 = synth.to_bf16(X)
         ms16, segs16, clk16 = measure(X16, args.steps, max(args.warmup, 3))
         del X16
+    # ---- N > 1 with the sharded output: the replicated output (every rank
+    # receives the whole aggregate, written by the producing kernels over
+    # NVLink) on the same step, after the timed region (both reported)
+    rep_ms = None
+    if world > 1 and args.output == "sharded" and not args.no_variants:
+        rep_out = "fused" if not bf16 else "replicated"
+        rep = {r: ShardedAggregator(r, n, f, d, output=rep_out, exchange=args.exchange) for r in RULES}
+        rep_ms, _, rep_clk = measure(X, args.steps, max(args.warmup, 3), A=rep)
+        t = torch.tensor([rep_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        rep_ms = float(t[0])
+        rep_path = rep[RULES[0]].fused_path
+        del rep
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -458,6 +474,12 @@ def run_ours(args):
     launches_per_step = 3 + 3 * (5 if peer else 4)
     stages = {c: round(t / args.steps, 4) for c, t in sorted(cls_ms.items())}
     per_rule = per_rule_table(rule_ms, es)
+    if rep_ms is not None:
+        variant = {"replicated_output": {
+            "what": "the same step with the aggregate replicated on every rank (output=" + rep_out
+                    + (f" ({rep_path})" if rep_path else "") + "), measured after this line's timed region",
+            "value": round(grad_bytes / (rep_ms / args.steps * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "ms_per_step": round(rep_ms / args.steps, 4), "clocks": rep_clk}}
     if world == 1 and not bf16 and not args.no_variants:
         ms16_step = ms16 / args.steps
         k16 = kernel_table(segs16, ms16_step, 2)
