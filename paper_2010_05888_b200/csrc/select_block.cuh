@@ -28,11 +28,71 @@ struct SelSmem {
   double sd[GAR_MAX_N][GAR_MAX_N];          // row i ascending, j != i
   unsigned char sj[GAR_MAX_N][GAR_MAX_N];
   double score[GAR_MAX_N];
+  double wbest[2][2];                       // Bulyan rounds, n > 32: the two warps' winners
+  int wbi[2][2];
   unsigned long long pool;
 };
 
 __device__ __forceinline__ bool key_lt(double a, int ia, double b, int ib) {
   return a < b || (a == b && ia < ib);
+}
+
+// Bulyan's theta rounds on W warps: thread i < n holds row i's distances in
+// ascending order (ROWS >= n - 1 registers) and their column indices; per
+// round, its score over the pool, then the argmin of (score, index): a warp
+// shuffle tree, and for W = 2 the two warp winners through shared memory
+// (one named barrier `bar2` of 64 threads per round, slots alternating).
+template <int ROWS, int W>
+__device__ __forceinline__ void bulyan_rounds(SelSmem& S, int n, int f, int theta, int32_t* __restrict__ idx_out,
+                                              int tid, int bar2) {
+  const int i = tid, lane = tid & 31, warp = tid >> 5;
+  double row[ROWS];
+  uint32_t rj4[(ROWS + 3) / 4];                    // column indices, 4 bytes per register
+#pragma unroll
+  for (int q = 0; q < (ROWS + 3) / 4; ++q) rj4[q] = 0;
+#pragma unroll
+  for (int e = 0; e < ROWS; ++e) {
+    const bool ok = i < n && e < n - 1;
+    row[e] = ok ? S.sd[i][e] : 0.0;
+    rj4[e >> 2] |= static_cast<uint32_t>(ok ? S.sj[i][e] : 0) << (8 * (e & 3));
+  }
+  unsigned long long P = (n == 64) ? ~0ull : ((1ull << n) - 1ull);
+  for (int t = 0; t < theta; ++t) {
+    const int k = max(__popcll(P) - f - 2, 0);
+    double sc = 0.0;
+    int taken = 0;
+#pragma unroll
+    for (int e = 0; e < ROWS; ++e) {
+      const int j = (rj4[e >> 2] >> (8 * (e & 3))) & 0xFF;
+      const bool take = e < n - 1 && ((P >> j) & 1ull) && taken < k;
+      if (take) sc += row[e];
+      taken += take ? 1 : 0;
+    }
+    const bool in = i < n && ((P >> i) & 1ull);
+    double best = in ? sc : INFINITY;
+    int bi = in ? i : (1 << 30);
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (key_lt(ob, oi, best, bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if constexpr (W == 2) {
+      const int slot = t & 1;
+      if (lane == 0) {
+        S.wbest[slot][warp] = best;
+        S.wbi[slot][warp] = bi;
+      }
+      gram::named_bar(bar2, 64);
+      const double b0 = S.wbest[slot][0], b1 = S.wbest[slot][1];
+      const int i0 = S.wbi[slot][0], i1 = S.wbi[slot][1];
+      bi = key_lt(b1, i1, b0, i0) ? i1 : i0;
+    }
+    if (i == 0) idx_out[t] = bi;
+    P &= ~(1ull << bi);
+  }
 }
 
 __device__ __forceinline__ void select_block(const double* __restrict__ G, int n, int f, int m, int rule,
@@ -91,90 +151,14 @@ __device__ __forceinline__ void select_block(const double* __restrict__ G, int n
   }
 
   const int theta = n - 2 * f;
+  // Bulyan: theta rounds of Krum with removal (R7).  Thread i (one warp for
+  // n <= 32, two for n <= 64) holds row i's sorted distances in registers;
+  // each round sums the k smallest pool members in ascending order (fp64, the
+  // oracle's additions) and an argmin over (score, index) picks the next.
   if (n <= 32) {
-    // Bulyan, n <= 32: one warp, lane i holds row i's sorted distances in
-    // registers; each round sums the k smallest pool members in ascending
-    // order (the same fp64 additions as below) and a shuffle argmin picks the
-    // lowest (score, index).  No block barriers.
-    if (tid < 32) {
-      const int i = tid;
-      double row[31];
-      int rj[31];
-#pragma unroll
-      for (int e = 0; e < 31; ++e) {
-        const bool ok = i < n && e < n - 1;
-        row[e] = ok ? sd[i][e] : 0.0;
-        rj[e] = ok ? sj[i][e] : 63;
-      }
-      unsigned long long P = (1ull << n) - 1ull;
-      for (int t = 0; t < theta; ++t) {
-        const int k = max(__popcll(P) - f - 2, 0);
-        double sc = 0.0;
-        int taken = 0;
-#pragma unroll
-        for (int e = 0; e < 31; ++e) {
-          const bool take = ((P >> rj[e]) & 1ull) && taken < k;
-          if (take) sc += row[e];
-          taken += take ? 1 : 0;
-        }
-        double best = (i < n && ((P >> i) & 1ull)) ? sc : INFINITY;
-        int bi = (i < n && ((P >> i) & 1ull)) ? i : (1 << 30);
-        for (int off = 16; off > 0; off >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-          if (key_lt(ob, oi, best, bi)) {
-            best = ob;
-            bi = oi;
-          }
-        }
-        if (i == 0) idx_out[t] = bi;
-        P &= ~(1ull << bi);
-      }
-    }
-    return;
-  }
-
-  // Bulyan: theta rounds of Krum with removal (R7)
-  for (int t = 0; t < theta; ++t) {
-    const unsigned long long P = pool;
-    const int psize = __popcll(P);
-    const int k = max(psize - f - 2, 0);
-    if (tid < n && ((P >> tid) & 1ull)) {
-      double s = 0.0;
-      int taken = 0;
-      for (int r = 0; r < n - 1 && taken < k; ++r) {
-        if ((P >> sj[tid][r]) & 1ull) {
-          s += sd[tid][r];
-          ++taken;
-        }
-      }
-      score[tid] = s;
-    }
-    named_bar(bar, nthreads);
-    if (tid < 32) {
-      // argmin over (score, index) in the pool: lanes cover i and i + 32
-      double best = INFINITY;
-      int bi = 1 << 30;
-      for (int i = tid; i < n; i += 32) {
-        if (((P >> i) & 1ull) && key_lt(score[i], i, best, bi)) {
-          best = score[i];
-          bi = i;
-        }
-      }
-      for (int off = 16; off > 0; off >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (key_lt(ob, oi, best, bi)) {
-          best = ob;
-          bi = oi;
-        }
-      }
-      if (tid == 0) {
-        idx_out[t] = bi;
-        pool = P & ~(1ull << bi);
-      }
-    }
-    named_bar(bar, nthreads);
+    if (tid < 32) bulyan_rounds<31, 1>(S, n, f, theta, idx_out, tid, bar + 1);
+  } else {
+    if (tid < 64) bulyan_rounds<63, 2>(S, n, f, theta, idx_out, tid, bar + 1);
   }
 }
 
