@@ -56,7 +56,7 @@ struct CfgCC {
   static constexpr int FLUSH_ST = 8;              // stages summed in fp32 per lane (32 coordinates)
   static constexpr int RAW_PITCH = RAW_KT * ES + 16;
   static constexpr int RAW_STAGES_MAX = 8;
-  static constexpr int SCRATCH = NP * 128 * 4 + NP * (NP + 1) * 4 + NP * 4;   // centre pick
+  static constexpr int SCRATCH = center_pick_bytes(NP);   // centre pick
   static constexpr int WSUM_BYTES = CONS_WARPS * NACC * 8;                    // per-warp fp64 sums
   static constexpr int SMEM_BYTES = 227 * 1024;
   static constexpr int BAR_BYTES = (PROD_WARPS + 1) * RAW_STAGES_MAX * 8 + 16;

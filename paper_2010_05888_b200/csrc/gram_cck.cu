@@ -59,7 +59,7 @@ struct CfgK {
   static constexpr int FLUSH_ST = 128 / (2 * STEPS);    // 128 coordinates per lane between flushes
   static constexpr int RAW_PITCH = RAW_KT * ES + 16;
   static constexpr int RAW_STAGES_MAX = 8;
-  static constexpr int PICK = NP * 128 * 4 + NP * (NP + 1) * 4 + NP * 4;
+  static constexpr int PICK = center_pick_bytes(NP);
   static constexpr int WSUM = WARPS * NACC * 8;
   static constexpr int SCRATCH = PICK > WSUM ? PICK : WSUM;   // wsum aliases the pick scratch
   static constexpr int SMEM_BYTES = 227 * 1024;

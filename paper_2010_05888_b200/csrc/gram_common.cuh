@@ -139,18 +139,25 @@ __device__ __forceinline__ uint32_t sw128_offset(int row, int c16) {
 // 128-coordinate sample of the CTA's slice, score_i = sum of the
 // floor((n-1)/2) smallest sample distances D_ij.  Deterministic.  `scratch`
 // (>= 49 KB of shared memory) is the idle operand ring.
+// sample rows are padded by 16 bytes: the pair loop's threads read different
+// rows at the same offset, conflict-free only if rows start in different banks
+constexpr int kPickS = 128, kPickPitch = kPickS + 4;       // sample coordinates, row pitch (floats)
+__host__ __device__ constexpr int center_pick_bytes(int np) {
+  return np * kPickPitch * 4 + np * (np + 1) * 4 + np * 4;
+}
+
 template <int NT, int NP, bool BF>
 __device__ int center_pick(const RowPtrs& rows, int n, int64_t d, int64_t k_begin, unsigned char* scratch) {
-  constexpr int S = 128;                                   // sample coordinates
-  float* xs = reinterpret_cast<float*>(scratch);           // [NP][S]
-  float* Ds = xs + NP * S;                                 // [NP][NP+1]
+  constexpr int S = kPickS, SP = kPickPitch;
+  float* xs = reinterpret_cast<float*>(scratch);           // [NP][SP]
+  float* Ds = xs + NP * SP;                                // [NP][NP+1]
   float* score = Ds + NP * (NP + 1);                       // [NP]
   if (n <= 2) return 0;
   const int t = threadIdx.x;
   for (int e = t; e < n * (S / 4); e += NT) {
     const int r = e / (S / 4), q = e % (S / 4);
     const float4 v = load_chunk_t<BF>(rows.p[r], k_begin + 4 * q, d);
-    reinterpret_cast<float4*>(xs + r * S)[q] = make_float4(fin(v.x), fin(v.y), fin(v.z), fin(v.w));
+    reinterpret_cast<float4*>(xs + r * SP)[q] = make_float4(fin(v.x), fin(v.y), fin(v.z), fin(v.w));
   }
   named_bar(3, NT);
   const int np = n * (n - 1) / 2;
@@ -158,8 +165,8 @@ __device__ int center_pick(const RowPtrs& rows, int n, int64_t d, int64_t k_begi
     int i = 0, u = p;
     while (u >= n - 1 - i) { u -= n - 1 - i; ++i; }
     const int j = i + 1 + u;
-    const float4* a = reinterpret_cast<const float4*>(xs + i * S);
-    const float4* b = reinterpret_cast<const float4*>(xs + j * S);
+    const float4* a = reinterpret_cast<const float4*>(xs + i * SP);
+    const float4* b = reinterpret_cast<const float4*>(xs + j * SP);
     float acc = 0.f;
     for (int k = 0; k < S / 4; ++k) {
       const float4 x = a[k], y = b[k];

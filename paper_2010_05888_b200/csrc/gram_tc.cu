@@ -119,7 +119,7 @@ struct Cfg {
   static_assert(RAW_REGION >= 2 * NP * RAW_PITCH, "two raw stages of NP rows");
   // the epilogue parks T/B over the (then idle) operand + raw rings
   static_assert(2 * NP * (NP + 1) * 8 <= OP_STAGES * OP_BYTES + RAW_REGION, "epilogue T/B parking space");
-  static_assert(NP * 128 * 4 + NP * (NP + 1) * 4 + NP * 4 <= OP_STAGES * OP_BYTES, "centre-pick scratch");
+  static_assert(center_pick_bytes(NP) <= OP_STAGES * OP_BYTES, "centre-pick scratch");
   static_assert(M == 128 && KB % 32 == 0, "tile shape");
 };
 
