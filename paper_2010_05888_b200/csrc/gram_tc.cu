@@ -36,7 +36,8 @@
 
 // GRAM_EXP (tools/gram_exp.sh only; 0 in the product): 1 = no MMAs issued,
 // 2 = converters skip the operand stores, 3 = converters skip all smem work,
-// 4 = 1 + 2.  Bottleneck attribution (profiles/r1_gram_experiments.md);
+// 4 = 1 + 2, 5 = converters skip the proxy fence.  Bottleneck attribution
+// (profiles/r1_gram_experiments.md, r2_gram_f16.md);
 // results are wrong by construction.
 #ifndef GRAM_EXP
 #define GRAM_EXP 0
@@ -53,6 +54,13 @@
 #endif
 #ifndef GRAM64_PROD
 #define GRAM64_PROD 3
+#endif
+// NP = 32 ring geometry (A/B knobs; defaults = product)
+#ifndef GRAM32_OPS
+#define GRAM32_OPS 2
+#endif
+#ifndef GRAM32_RAW_SUB
+#define GRAM32_RAW_SUB 3
 #endif
 
 namespace gar {
@@ -86,13 +94,13 @@ struct Cfg {
   static constexpr int ATOMS = KB / 32;          // 128-byte K atoms per tile
   static constexpr int ATOM_BYTES = M * 128;     // one K atom of A (8-row groups of 1 KB)
   static constexpr int OP_BYTES = ATOMS * ATOM_BYTES;      // one operand stage (A; B aliases its H rows)
-  static constexpr int OP_STAGES = (NP == 64) ? GRAM64_OPS : 2;
+  static constexpr int OP_STAGES = (NP == 64) ? GRAM64_OPS : (NP == 32) ? GRAM32_OPS : 2;
   // Raw ring: one TMA bulk copy per row covers RAW_SUB tiles (1.5 KB / 1 KB per
   // row), issued by PROD_WARPS warps (rows r = p mod PROD_WARPS, one barrier
   // each): bulk-copy issue is limited per request and per issuing warp
   // (tools/membench.cu, membench2.cu).
   static constexpr int PROD_WARPS = (NP == 64) ? GRAM64_PROD : 3;     // 5 or 7 for NP = 64 measured slower (tools/gram_exp.sh)
-  static constexpr int RAW_SUB = (NP == 8) ? 1 : (NP == 16) ? 2 : (NP == 32) ? 3 : GRAM64_RAW_SUB;   // 2 / 2 / 1.5 / 1 KB per row
+  static constexpr int RAW_SUB = (NP == 8) ? 1 : (NP == 16) ? 2 : (NP == 32) ? GRAM32_RAW_SUB : GRAM64_RAW_SUB;   // 2 / 2 / 1.5 / 1 KB per row
   static constexpr int RAW_KT = RAW_SUB * KT;    // coordinates per raw stage
   // bytes per raw row (+16: conflict-free LDS.128 per 8-lane phase for fp32
   // and for bf16 at CH >= 2, LDS.64 per 16-lane phase for bf16 at CH = 1)
@@ -377,7 +385,7 @@ __global__ void __launch_bounds__(Cfg<NP, BF>::THREADS, 1)
             }
           }
         }
-        fence_proxy_async_smem();
+        if (GRAM_EXP != 5) fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&op_full[s]);
       }
