@@ -23,6 +23,15 @@
 #include "elem.cuh"
 #include "networks.cuh"
 
+// A/B knobs (defaults = product): consumer warps of the Bulyan phase up to 32
+// rows, and the TMA ring budget in KB
+#ifndef GAR_BULYAN_W
+#define GAR_BULYAN_W 24
+#endif
+#ifndef GAR_RING_KB
+#define GAR_RING_KB 200
+#endif
+
 namespace gar {
 
 // W consumer warps (one coordinate per thread per tile) + kProducers producer
@@ -47,7 +56,8 @@ template <int MODE, int N>
 constexpr int consumer_warps() {
   if constexpr (N > 48) return 12;
   if constexpr (N > 32) return MODE == kModeTrimmed ? 16 : 12;
-  return (MODE == kModeTrimmed || MODE == kModeBulyan) ? 24 : 15;
+  if constexpr (MODE == kModeBulyan) return GAR_BULYAN_W;
+  return MODE == kModeTrimmed ? 24 : 15;
 }
 
 struct CoordParams {
@@ -625,7 +635,7 @@ inline cudaError_t launch_mode_w(const CoordLaunch& L, cudaStream_t stream) {
   p.R = L.R;
   p.f = L.f;
   const size_t stage_bytes = size_t(L.R) * kTile * sizeof(T);
-  int stages = static_cast<int>((200 * 1024) / stage_bytes);
+  int stages = static_cast<int>((GAR_RING_KB * 1024) / stage_bytes);
   stages = max(2, min(8, stages));
   p.stages = stages;
   p.l2_hint = l2_evict_first_enabled();

@@ -6,7 +6,7 @@
 set -e
 name=$1; src=$(realpath $2); shift 2
 base=$(basename $src .cu); base=${base%%_r1}; base=${base%%_tf32}
-case $base in gram_f16*) obj=gram_f16.o ;; *) obj=gram_tc.o ;; esac
+case $base in gram_f16*) obj=gram_f16.o ;; gram_tc*) obj=gram_tc.o ;; *) obj=$base.o ;; esac
 cd /root/repo/paper_2010_05888_b200
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
   --expt-relaxed-constexpr -I csrc -I ../include "$@" -c $src -o /tmp/gram_$name.o
