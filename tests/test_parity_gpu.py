@@ -414,6 +414,44 @@ def test_distances_parity(gar):
         distances_close(D.cpu().numpy(), oracle.distances(x))
 
 
+def _distances_within_norm_bound(D_gpu, x, D_ref, rel=1e-5):
+    """The Gram method's error bound: fp32 products of centred rows, so the
+    error of D_ij is relative to the centred squared norms, not to D_ij (with
+    one coordinate, two nearly equal rows give a tiny D_ij by cancellation).
+    Bound the kernel's centring row r* by the worst row: |x_i - c|^2 <=
+    2 (|x_i - m|^2 + max_r |x_r - m|^2), m the coordinate-wise median."""
+    xd = x.astype(np.float64)
+    nrm = ((xd - np.median(xd, axis=0)) ** 2).sum(axis=1)
+    scale = 2.0 * (nrm[:, None] + nrm[None, :] + 2.0 * nrm.max())
+    err = np.abs(D_gpu - D_ref)
+    assert np.all(err <= rel * (D_ref + scale)), f"max err / bound {np.max(err / (rel * (D_ref + scale) + 1e-300)):.3e}"
+
+
+@pytest.mark.parametrize("n", list(range(2, 26)))
+def test_distances_every_small_n(gar, n):
+    """Every n served by an exact-n CUDA-core Gram instantiation (n <= 15: all
+    pairs per lane; 16..22: two pair chunks) and the tensor-core boundary
+    (23..25), at d values that leave ragged stages and tails (not multiples of
+    the 1536 / 896 / 512-coordinate stages, nor of 4), fp32 rows and bf16 rows
+    (widened exactly, R16).  d >= 4099: D within 1e-5 relative of the oracle;
+    d = 1 (the global-load tail path only, where near-equal rows make D_ij a
+    cancellation): within 1e-5 of the centred norms."""
+    for d in (1, 4099, 30_011):
+        x = synth.make_gradients(n, (n - 3) // 4 if n >= 3 else 0, d, seed=900 + n, ld=d).numpy()
+        ws = torch.empty(gar.gar_workspace_bytes("krum", max(n, 3), 0, d), dtype=torch.uint8, device="cuda")
+        D = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        xb = synth.to_bf16(torch.from_numpy(x))
+        xw = oracle.widen_bf16(synth.bf16_bits(xb))[:, :d]
+        for rows, ref_rows, call in ((to_device(x), x, gar.gar_distances), (xb.cuda(), xw, gar.gar_distances_dt)):
+            call(rows, D, ws, d=d)
+            torch.cuda.synchronize()
+            Dg, Do = D.cpu().numpy(), oracle.distances(ref_rows)
+            if d == 1:
+                _distances_within_norm_bound(Dg, ref_rows, Do)
+            else:
+                distances_close(Dg, Do)
+
+
 def test_distances_nonfinite(gar):
     x = np.random.default_rng(0).standard_normal((9, 1000)).astype(np.float32)
     x[3, 17] = np.nan
