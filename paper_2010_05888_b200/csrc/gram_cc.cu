@@ -30,6 +30,10 @@
 #include "gram.h"
 #include "gram_common.cuh"
 
+#ifndef GAR_CC_FLUSH
+#define GAR_CC_FLUSH 8   // A/B knob (default = product)
+#endif
+
 namespace gar {
 
 namespace {
@@ -53,7 +57,7 @@ struct CfgCC {
   static constexpr int RAW_KT = CONS_WARPS * 128;       // coordinates per raw stage
   static constexpr int PART = RAW_KT / CONS_WARPS;      // 128 coordinates per warp and stage
   static constexpr int PER_LANE = PART / 32;            // 4
-  static constexpr int FLUSH_ST = 8;              // stages summed in fp32 per lane (32 coordinates)
+  static constexpr int FLUSH_ST = GAR_CC_FLUSH;   // stages summed in fp32 per lane (4 coordinates each)
   static constexpr int RAW_PITCH = RAW_KT * ES + 16;
   static constexpr int RAW_STAGES_MAX = 8;
   static constexpr int SCRATCH = center_pick_bytes(NP);   // centre pick
