@@ -14,12 +14,13 @@
 // Layout (n <= 15, every loop unrolled for the exact n): each element is read
 // from the TMA ring once; a lane keeps all n(n+1)/2 products-sums of the
 // coordinates it visits (consumer warp w owns part w of every raw stage, lane
-// l its coordinates l, l+32, ...), in fp32 over FLUSH_ST stages (32 coordinates
+// l its coordinates l, l+32, ...), in fp32 over FLUSH_ST stages (128 coordinates
 // per lane); then a butterfly (transpose-)reduction over the 32 lanes leaves
 // each lane NACC/32 of the entries, added into fp64; warps are summed in fixed
-// order at the end (deterministic).  Precision: <= 32 fp32 FFMAs per lane plus
-// 5 butterfly levels before each fp64 add, i.e. <= ~37 * 2^-24 of the flushed
-// |products| (measured D errors ~1e-8 relative, tools/check_gram.py).
+// order at the end (deterministic).  Precision: <= 128 fp32 FFMAs per lane plus
+// 5 butterfly levels before each fp64 add, i.e. <= ~133 * 2^-24 of the flushed
+// |products|, the class of the tf32 kernel's 128-product TMEM drains (measured
+// D errors ~1e-8 relative, tools/check_gram.py).
 #include <cmath>
 #include <cstdint>
 #include <type_traits>
@@ -31,7 +32,7 @@
 #include "gram_common.cuh"
 
 #ifndef GAR_CC_FLUSH
-#define GAR_CC_FLUSH 8   // A/B knob (default = product)
+#define GAR_CC_FLUSH 32   // A/B knob (default = product; 8 -> 32: n = 15 0.256 -> 0.246 ms)
 #endif
 
 namespace gar {
