@@ -35,6 +35,11 @@ cudaError_t launch_gram_cc(const float* const* rows, int n, int64_t d, double* p
 // kGramCckMaxN.
 constexpr int kGramCckLimit = 22;
 constexpr int kGramCckMaxN = 22;
+// ... and register-blocked over 8 warps (4 row groups of S = 9: 6 block units,
+// 2 triangle-pair units; gram_ccb.cuh) for kGramCcbMinN <= n <= kGramCcbMaxN,
+// where it beats the NP = 64 tensor-core pass (1.05 vs 1.27 ms at n = 35)
+constexpr int kGramCcbMinN = 33;
+constexpr int kGramCcbMaxN = 36;
 cudaError_t launch_gram_cck(const float* const* rows, int n, int64_t d, double* partials, int num_sms,
                             int* n_parts, cudaStream_t stream, int dtype);
 

@@ -1,14 +1,13 @@
 // gram_ccb.cuh — the pairwise-distance contraction on the CUDA cores for
-// kGramCcMaxN < n <= kGramCcbLimit rows: per-CTA partial Gram
-// matrices of the centred rows, G_ij = sum_k (x_ik - c_k)(x_jk - c_k), the
-// contract of gram_tc.cu / gram_cc.cu.
+// kGramCcbMinN <= n <= kGramCcbMaxN rows (33..36): per-CTA
+// partial Gram matrices of the centred rows, G_ij = sum_k (x_ik - c_k)(x_jk -
+// c_k), the contract of gram_tc.cu / gram_cc.cu.
 //
-// Why: the tensor-core Gram is bound by per-tile shared-memory traffic and the
-// N = 64 MMA issue cost, which do not shrink with n (NP = 64 for 33..64 rows:
-// 1.28 ms at n = 35 against 0.55 ms of HBM time).  The contraction itself is
-// n(n+1)/2 FFMA per coordinate; at the HBM rate an SM has ~22.8 n issue slots
-// per coordinate, so FFMA at full issue efficiency stays under the memory time
-// up to n ~ 45.  What decides is how few non-FFMA instructions surround them.
+// Why: from 33 rows the tensor-core Gram pads to NP = 64 and is bound by the
+// N = 64 MMA issue cost and its padded operand traffic (1.27 ms at n = 35
+// against 0.55 ms of HBM time).  Here the n(n+1)/2 products per coordinate run
+// as FFMA: 1.05 ms at S = 9 (n = 33..36); from S = 10 (n >= 37) and below
+// n = 33 the tensor cores win again (profiles/r2_gram_cc.md).
 //
 // Register blocking.  Rows in 4 groups of S = ceil(n/4) (the last group padded
 // with zero rows that live in every ring slot); the upper triangle of G in 8
@@ -36,6 +35,10 @@
 #include "gram.h"
 #include "gram_common.cuh"
 
+#ifndef GAR_CCB_KT
+#define GAR_CCB_KT 512
+#endif
+
 namespace gar {
 namespace ccb {
 
@@ -53,12 +56,12 @@ struct Cfg {
   static constexpr int THREADS = WARPS * 32;
   static constexpr int NACC_OFF = (S * S + 31) / 32 * 32;        // block unit accumulators
   static constexpr int NACC_DIAG = (S * (S + 1) + 31) / 32 * 32;  // triangle-pair unit accumulators
-  static constexpr int RAW_KT = N <= 24 ? 512 : 256;         // coordinates per stage
+  static constexpr int RAW_KT = GAR_CCB_KT;                  // coordinates per stage
   static constexpr int PER_LANE = RAW_KT / 64;               // coordinate pairs per lane and stage
   static constexpr int FLUSH_ST = 128 * 32 / RAW_KT;         // 128 coordinates per lane between flushes
   static constexpr int RAW_PITCH = RAW_KT * ES + 16;
   static constexpr int RAW_STAGES_MAX = 8;
-  static constexpr int PICK = NP * 128 * 4 + NP * (NP + 1) * 4 + NP * 4;   // centre pick scratch
+  static constexpr int PICK = center_pick_bytes(NP);                      // centre pick scratch
   static constexpr int WSUM = WARPS * NACC_DIAG * 8;                      // fp64 unit sums (aliases PICK)
   static constexpr int SCRATCH = PICK > WSUM ? PICK : WSUM;
   static constexpr int SMEM_BYTES = 227 * 1024;
@@ -154,7 +157,7 @@ struct Slice {
 // 1.5 n instructions instead of one FSUB per unit row (4 n).  Same arithmetic
 // (one __fsub_rn per element), bit-identical result.
 #ifndef GAR_CCB_PRE
-#define GAR_CCB_PRE 1
+#define GAR_CCB_PRE 0
 #endif
 
 template <int N>
@@ -260,21 +263,21 @@ __device__ __forceinline__ void consume(const RowPtrs& rows, const Slice& sl, un
     const unsigned char* rJ = st + J0 * C::RAW_PITCH;
     const unsigned char* rC = st + rc * C::RAW_PITCH;
     if (k0 + C::RAW_KT <= sl.d_bulk) {          // a full stage, all of it in the ring
-      // two coordinate pairs per trip, the loads of the next pair issued
-      // before the products of this one (2 warps per SM sub-partition cannot
-      // hide shared-memory latency otherwise)
-      float2 aI[S], aJ[S], bI[S], bJ[S], ac, bc;
-      auto load = [&](int t, float2* vI, float2* vJ, float2& c2) {
+#pragma unroll 1
+      for (int t = 0; t < C::PER_LANE; ++t) {
         const int k = 2 * lane + 64 * t;
+        float2 vI[S], vJ[S];
 #pragma unroll
         for (int a = 0; a < S; ++a) vI[a] = ld_pair<BF>(rI + a * C::RAW_PITCH, k);
 #pragma unroll
         for (int b = 0; b < S; ++b) vJ[b] = ld_pair<BF>(rJ + b * C::RAW_PITCH, k);
-        if constexpr (!PRE) c2 = ld_pair<BF>(rC, k);
-      };
-      auto products = [&](const float2* vI, const float2* vJ, float2 c2) {
         float hI[S], hJ[S];
-        const float cx = PRE ? 0.f : fin(c2.x), cy = PRE ? 0.f : fin(c2.y);
+        float cx = 0.f, cy = 0.f;
+        if constexpr (!PRE) {
+          const float2 c2 = ld_pair<BF>(rC, k);
+          cx = fin(c2.x);
+          cy = fin(c2.y);
+        }
 #pragma unroll
         for (int a = 0; a < S; ++a) hI[a] = PRE ? vI[a].x : __fsub_rn(vI[a].x, cx);
 #pragma unroll
@@ -285,15 +288,6 @@ __device__ __forceinline__ void consume(const RowPtrs& rows, const Slice& sl, un
 #pragma unroll
         for (int b = 0; b < S; ++b) hJ[b] = PRE ? vJ[b].y : __fsub_rn(vJ[b].y, cy);
         unit_fma<S, DIAG>(acc, hI, hJ);
-      };
-      static_assert(C::PER_LANE % 2 == 0, "pairs of trips");
-      load(0, aI, aJ, ac);
-#pragma unroll 1
-      for (int t = 0; t < C::PER_LANE; t += 2) {
-        load(t + 1, bI, bJ, bc);
-        products(aI, aJ, ac);
-        if (t + 2 < C::PER_LANE) load(t + 2, aI, aJ, ac);
-        products(bI, bJ, bc);
       }
     } else {                                     // the slice's last stage: ragged, tail from global
       const int cnt = static_cast<int>((sl.k_end - k0 < C::RAW_KT) ? sl.k_end - k0 : C::RAW_KT);

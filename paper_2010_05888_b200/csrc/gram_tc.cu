@@ -527,9 +527,16 @@ cudaError_t launch_gram_t(const float* const* rows, int n, int64_t d, double* pa
 
 }  // namespace
 
+// register-blocked CUDA-core Gram (gram_ccb.cuh, gram_ccb_{f32,bf16}.cu)
+cudaError_t launch_gram_ccb_f32(const RowPtrs& rp, int n, int64_t d, double* partials, int num_sms, int* n_parts,
+                                cudaStream_t stream);
+cudaError_t launch_gram_ccb_bf16(const RowPtrs& rp, int n, int64_t d, double* partials, int num_sms, int* n_parts,
+                                 cudaStream_t stream);
+
 // Kernel choice: CUDA-core FFMA Gram (gram_cc.cu n <= kGramCcMaxN, gram_cck.cu
-// n <= kGramCckMaxN), the tensor-core kernel above (and for the fused ingress
-// staging, which only the tensor-core kernel implements).  GAR_GRAM_CC=0
+// n <= kGramCckMaxN, gram_ccb.cuh kGramCcbMinN..kGramCcbMaxN), the tensor-core
+// kernel elsewhere (and for the fused ingress staging, which only the
+// tensor-core kernel implements).  GAR_GRAM_CC=0
 // forces the tensor cores, =1 the CUDA cores up to kGramCckLimit (A/B).
 static int gram_cc_forced() {
   static const int v = [] {
@@ -544,6 +551,12 @@ cudaError_t launch_gram_partials(const float* const* rows, int n, int64_t d, dou
   const int forced = gram_cc_forced();
   if (!stage_rows && forced != 0) {
     if (n <= kGramCcMaxN) return launch_gram_cc(rows, n, d, partials, num_sms, n_parts, stream, dtype);
+    if (n >= kGramCcbMinN && n <= kGramCcbMaxN) {
+      RowPtrs rp;
+      for (int i = 0; i < GAR_MAX_N; ++i) rp.p[i] = (i < n) ? rows[i] : nullptr;
+      return dtype == kBF16 ? launch_gram_ccb_bf16(rp, n, d, partials, num_sms, n_parts, stream)
+                            : launch_gram_ccb_f32(rp, n, d, partials, num_sms, n_parts, stream);
+    }
     if (n <= (forced == 1 ? kGramCckLimit : kGramCckMaxN))
       return launch_gram_cck(rows, n, d, partials, num_sms, n_parts, stream, dtype);
   }
