@@ -33,8 +33,8 @@ cudaError_t launch_gram_cc(const float* const* rows, int n, int64_t d, double* p
 // ... and for kGramCcMaxN < n <= kGramCckLimit with the pair triangle cut into
 // two chunks over warps (gram_cck.cu); launch_gram_partials uses it up to
 // kGramCckMaxN.
-constexpr int kGramCckLimit = 22;
-constexpr int kGramCckMaxN = 22;
+constexpr int kGramCckLimit = 24;
+constexpr int kGramCckMaxN = 24;
 // ... and register-blocked over 8 warps (4 row groups of S = 9: 6 block units,
 // 2 triangle-pair units; gram_ccb.cuh) for kGramCcbMinN <= n <= kGramCcbMaxN,
 // where it beats the NP = 64 tensor-core pass (1.05 vs 1.27 ms at n = 35)

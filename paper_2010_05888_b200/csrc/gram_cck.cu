@@ -56,7 +56,12 @@ struct CfgK {
   static constexpr int BULK_ALIGN = 16 / ES;
   static constexpr int NPAIR = N * (N + 1) / 2;
   static constexpr int CH = (NPAIR + K - 1) / K;        // pairs per chunk
-  static constexpr int NACC = (CH + 31) / 32 * 32;
+  // sums per lane: up to 128 padded to a multiple of 32 (all through the
+  // butterfly); above, 128 through the butterfly + NREM < 32 reduced one by one
+  // (a 160-entry array goes to local memory)
+  static constexpr int NBUT = CH <= 128 ? (CH + 31) / 32 * 32 : 128;
+  static constexpr int NREM = CH <= 128 ? 0 : CH - 128;
+  static constexpr int NACC = NBUT + NREM;
   static constexpr int STEPS = GAR_CCK_STEPS;           // coordinate pairs per lane and stage
   static constexpr int PART = 64 * STEPS;               // coordinates per warp and stage
   static constexpr int RAW_KT = P * PART;
@@ -69,7 +74,7 @@ struct CfgK {
   static constexpr int SMEM_BYTES = 227 * 1024;
   static constexpr int BAR_BYTES = RAW_STAGES_MAX * 8 + 16;
   static constexpr int RAW_REGION = SMEM_BYTES - 128 - SCRATCH - BAR_BYTES;
-  static_assert(NACC <= 128, "<= 128 accumulators per lane (160 go to local memory)");
+  static_assert(NREM < 32, "at most 159 sums per lane");
   static_assert(RAW_REGION >= 2 * N * RAW_PITCH, "two raw stages");
 };
 
@@ -168,9 +173,10 @@ __device__ __forceinline__ void consume_k(const RowPtrs& rows, const SliceK& sl,
   float acc[C::NACC];
 #pragma unroll
   for (int e = 0; e < C::NACC; ++e) acc[e] = 0.f;
-  double acc64[C::NACC / 32];
+  double acc64[C::NBUT / 32];
 #pragma unroll
-  for (int t = 0; t < C::NACC / 32; ++t) acc64[t] = 0.0;
+  for (int t = 0; t < C::NBUT / 32; ++t) acc64[t] = 0.0;
+  double accr = 0.0;                                   // remainder entry NBUT + lane (lane < NREM)
   for (int64_t j = 0; j < sl.S && j < raw_stages; ++j)
     issue_stage_k<N, BF>(rows, sl, raw + j * raw_bytes, &full[j], j, warp, lane, pol, l2_hint);
   int rs = 0, fl = 0;
@@ -219,16 +225,25 @@ __device__ __forceinline__ void consume_k(const RowPtrs& rows, const SliceK& sl,
     if (j + raw_stages < sl.S)
       issue_stage_k<N, BF>(rows, sl, st, &full[rs], j + raw_stages, warp, lane, pol, l2_hint);
     if (++fl == C::FLUSH_ST || j + 1 == sl.S) {
-      flush_k<C::NACC>(acc, acc64, lane);
+      flush_k<C::NBUT>(acc, acc64, lane);
+#pragma unroll
+      for (int e = 0; e < C::NREM; ++e) {              // fixed xor tree: every lane holds the sum
+        float v = acc[C::NBUT + e];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == e) accr += static_cast<double>(v);
+        acc[C::NBUT + e] = 0.f;
+      }
       fl = 0;
     }
     if (++rs == raw_stages) rs = 0, ph ^= 1;
   }
   int eb = 0;
-  for (int o = 16, half = C::NACC / 2; o >= 1; o >>= 1, half >>= 1) eb += (lane & o) ? half : 0;
+  for (int o = 16, half = C::NBUT / 2; o >= 1; o >>= 1, half >>= 1) eb += (lane & o) ? half : 0;
   // wsum aliases the centre-pick scratch, free since the kernel's __syncthreads
 #pragma unroll
-  for (int t = 0; t < C::NACC / 32; ++t) wsum[warp * C::NACC + eb + t] = acc64[t];
+  for (int t = 0; t < C::NBUT / 32; ++t) wsum[warp * C::NACC + eb + t] = acc64[t];
+  if (lane < C::NREM) wsum[warp * C::NACC + C::NBUT + lane] = accr;
 }
 
 template <int N, bool BF, int CK = 0>

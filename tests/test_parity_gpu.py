@@ -259,7 +259,7 @@ def test_mean_around_median_parity(gar, n, f):
     assert_same_bits(out.cpu().numpy(), oracle.mean_around_median(x, f), "mean around median")
 
 
-GRAM_CC_MAX_N = 22   # csrc/gram.h kGramCckMaxN: the CUDA-core Gram up to it (and for 33..36), the tensor cores above
+GRAM_CC_MAX_N = 24   # csrc/gram.h kGramCckMaxN: the CUDA-core Gram up to it (and for 33..36), the tensor cores above
 
 
 @pytest.mark.parametrize("n,d", [(7, 100_003), (15, 100_003), (19, 100_003), (31, 300_001), (35, 50_003), (64, 20_003)])
@@ -267,7 +267,7 @@ def test_gram_exchange_single_rank_and_staging(gar, n, d):
     """gar_gram_exchange with world = 1 (slots and flags in this GPU's memory):
     the flag handshake completes, G equals gar_gram_partial's bit for bit, and
     the staging copy (the fused ingress of the d-sharded path) equals the rows.
-    The staging copy exists only in the tensor-core Gram, so for n <= 22 a
+    The staging copy exists only in the tensor-core Gram, so for n <= 24 a
     staged exchange runs the other kernel than gar_gram_partial: equal there
     in D within the 1e-5 bar."""
     x = synth.make_gradients(n, (n - 3) // 4 if n >= 3 else 0, d, seed=5 + n, ld=d).numpy()
@@ -427,11 +427,11 @@ def _distances_within_norm_bound(D_gpu, x, D_ref, rel=1e-5):
     assert np.all(err <= rel * (D_ref + scale)), f"max err / bound {np.max(err / (rel * (D_ref + scale) + 1e-300)):.3e}"
 
 
-@pytest.mark.parametrize("n", list(range(2, 26)) + [32, 33, 34, 35, 36, 37])
+@pytest.mark.parametrize("n", list(range(2, 27)) + [32, 33, 34, 35, 36, 37])
 def test_distances_every_small_n(gar, n):
     """Every n served by an exact-n CUDA-core Gram instantiation (n <= 15: all
-    pairs per lane; 16..22: two pair chunks; 33..36: register blocks) and the
-    tensor-core boundaries (23..25, 32, 37), at d values that leave ragged stages and tails (not multiples of
+    pairs per lane; 16..24: two pair chunks; 33..36: register blocks) and the
+    tensor-core boundaries (25, 32, 37), at d values that leave ragged stages and tails (not multiples of
     the 1536 / 896 / 512-coordinate stages, nor of 4), fp32 rows and bf16 rows
     (widened exactly, R16).  d >= 4099: D within 1e-5 relative of the oracle;
     d = 1 (the global-load tail path only, where near-equal rows make D_ij a
